@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""bench.py — SRT3D hot path on B200: one step = sketch one synthetic frame
+(Eq. 3) + the config's sketched-gradient iterations (Eq. 6/8 data step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5]
+                  [--n-per-pixel 1000000 (C4 only)] [--impl srt3d|reference]
+
+Default workload: BASELINE.json configs[4] (C5: 512x512 px, T=8192, K=3,
+1000 photons/px at SBR 0.01, m=32, 200 iterations) — the largest config that
+exercises both kernels (DESIGN.md §7 explains the choice).  Inputs are
+seeded synthetic frames (srt3d_inputs) standing in for the paper's datasets.
+
+Multi-GPU (torchrun): pixels are independent (no data-path collective);
+every rank processes its own frame of the same config ("scaling": "weak"),
+timed with CUDA events between barriers, max over ranks.
+
+Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle on
+the host cores instead (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP32_LANES_PER_SM = 128  # FP32 FMA lanes per SM (B200)
+METRIC = "photons/s sketched (GB/s vs HBM peak); sketched-gradient pixel-iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="srt3d", choices=["srt3d", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n-per-pixel", type=int, default=1000000, help="C4 photons per pixel")
+    ap.add_argument("--unfused", action="store_true", help="separate grad + update kernels")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index: int):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+        time.sleep(0.25)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ oracle (CPU)
+def oracle_step_sample(frame, seconds: float, rank0_only=True):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the frame:
+    sketch of npix_s pixels + the config's iterations on those pixels."""
+    import oracle
+
+    oracle.build()
+    cores = oracle.max_threads()
+
+    def run(npix_s):
+        idx = np.arange(npix_s)
+        offs = frame.offsets[: npix_s + 1].astype(np.int64)
+        bins = frame.bins[offs[0]:offs[-1]]
+        offs = (offs - offs[0]).astype(np.uint32)
+        t0, a0 = frame.theta0()
+        t, a = t0[idx].astype(np.float64), a0[idx].astype(np.float64)
+        t_start = time.perf_counter()
+        z = oracle.sketch(bins, offs, frame.T, frame.m)
+        for _ in range(frame.iters):
+            gt, ga, _ = oracle.sketch_grad(z, t, a, frame.sigma, frame.T, frame.m)
+            t, a = oracle.descent_update(t, a, gt, ga, frame.sigma, frame.T, frame.m, eta=0.5)
+        dt = time.perf_counter() - t_start
+        return dt, int(offs[-1])
+
+    n = min(frame.npix, 64)
+    dt, ph = run(n)
+    while dt < 0.05 * seconds and n < frame.npix:
+        n = min(frame.npix, n * 4)
+        dt, ph = run(n)
+    if dt < seconds and n < frame.npix:
+        n = min(frame.npix, max(n, int(n * seconds / max(dt, 1e-6))))
+        dt, ph = run(n)
+    return {"seconds": dt, "photons": ph, "pixels": n, "cores": cores,
+            "sample": f"first {n} of {frame.npix} pixels ({ph} photons): oracle sketch + {frame.iters} "
+                      f"fp64 gradient/update iterations"}
+
+
+def make_frame(args, rank: int):
+    import srt3d_inputs
+
+    if args.config == "C4":
+        f = srt3d_inputs.make_frame("C4", n_per_pixel=args.n_per_pixel,
+                                    seed=None if rank == 0 else 104 + 1000 * rank)
+    else:
+        seed = None if rank == 0 else srt3d_inputs.CONFIGS[args.config]["seed"] + 1000 * rank
+        f = srt3d_inputs.make_frame(args.config, seed=seed)
+    return f
+
+
+def config_obj(f, args):
+    return {"workload": f"{f.name}: {f.rows}x{f.cols} px, T={f.T}, K={f.K}, m={f.m}, sigma={f.sigma}, "
+                        f"{'fixed ' + str(args.n_per_pixel) if args.config == 'C4' else 'Poisson mean ' + str(f.lam)}"
+                        f" photons/px, SBR={f.sbr}, {f.iters} gradient iterations",
+            "npix": f.npix, "photons_per_frame": f.n_photons, "T": f.T, "m": f.m, "K": f.K, "sigma": f.sigma,
+            "iters": f.iters, "seed": f.seed, "recipe": f.recipe,
+            "l2": "photon input per step larger than L2 (not flushed); z/theta stay L2-resident across iterations",
+            "parallelism": f"dp{args.gpus} (independent frames per GPU)"}
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    f = make_frame(args, 0)
+    per_step = max(1.0, args.cpu_seconds / max(args.steps, 1))
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        oracle_step_sample(f, min(per_step, 1.0))
+    times, photons, info = [], [], None
+    for _ in range(args.steps):
+        info = oracle_step_sample(f, per_step)
+        times.append(info["seconds"])
+        photons.append(info["photons"])
+    value = sum(photons) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "photons/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_obj(f, args),
+            "cpu_baseline": {"value": value, "unit": "photons/s", "cores": info["cores"], "kind": "oracle",
+                             "sample": info["sample"]},
+            "e2e": {"value": value, "unit": "photons/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_srt3d(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_00952_b200 as srt3d
+    from paper_2203_00952_b200.pipeline import FramePipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    srt3d.load_library()
+    f = make_frame(args, rank)
+    pipe = FramePipeline(f.n_photons, f.npix, f.K, f.T, f.m, f.sigma, f.iters, fused=not args.unfused,
+                         use_graphs=not args.no_graph)
+    bins_h = torch.from_numpy(f.bins)
+    offs_h = torch.from_numpy(f.offsets)
+    t0_h, a0_h = (torch.from_numpy(x) for x in f.theta0())
+    pipe.load_device(bins_h, offs_h, t0_h, a0_h)
+    pipe.capture()
+    s = pipe.stream
+
+    for _ in range(args.warmup):
+        pipe.run_device()
+    s.synchronize()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(s)
+    for k in range(args.steps):
+        ev[k][0].record(s)
+        pipe.sketch_phase()
+        ev[k][1].record(s)
+        pipe.iterate_phase()
+        ev[k][2].record(s)
+    end.record(s)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = start.elapsed_time(end)
+    sk_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    it_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    photons_all = f.n_photons * args.steps * world  # weak scaling: every rank its own frame
+
+    # end-to-end through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        bins_p, offs_p = bins_h.pin_memory(), offs_h.pin_memory()
+        t0_p, a0_p = t0_h.pin_memory(), a0_h.pin_memory()
+        t_out, a_out = torch.empty_like(t0_p).pin_memory(), torch.empty_like(a0_p).pin_memory()
+        pipe.run_host(bins_p, offs_p, t0_p, a0_p, t_out, a_out)
+        s.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(args.e2e_steps):
+            pipe.run_host(bins_p, offs_p, t0_p, a0_p, t_out, a_out)
+        e1.record(s)
+        s.synchronize()
+        barrier()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": f.n_photons * args.e2e_steps * world / (float(e2e_ms.item()) * 1e-3), "unit": "photons/s",
+               "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
+               "ms_per_step": float(e2e_ms.item()) / args.e2e_steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peaks, peak_kind = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6547.8))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    fp32_peak = nsm * FP32_LANES_PER_SM * 2 * sm_max * 1e6  # flop/s at max clock
+    sk_avg = statistics.mean(sk_ms)
+    it_avg = statistics.mean(it_ms)
+    # sketch: F = 8 m n flops, B = 2n + 4 npix + 8 m npix bytes
+    sk_flops = 8.0 * f.m * f.n_photons
+    sk_bytes = 2.0 * f.n_photons + 4.0 * (f.npix + 1) + 8.0 * f.m * f.npix
+    sketch = {"kernel": "srt3d_sketch", "ms": sk_avg, "photons_per_s": f.n_photons / (sk_avg * 1e-3),
+              "gbs": sk_bytes / (sk_avg * 1e-3) / 1e9, "tflops": sk_flops / (sk_avg * 1e-3) / 1e12,
+              "frac_fp32": (sk_flops / (sk_avg * 1e-3)) / fp32_peak,
+              "frac_hbm": (sk_bytes / (sk_avg * 1e-3) / 1e9) / hbm}
+    grad = None
+    if f.iters > 0:
+        per_iter = it_avg / f.iters
+        # fused step per pixel-iteration: read z (8m) + t, alpha (8K); write t, alpha (8K)
+        g_bytes = f.npix * (8.0 * f.m + 16.0 * f.K) if pipe.fused else f.npix * (8.0 * f.m + 32.0 * f.K + 16.0 * f.K)
+        g_flops = f.npix * (21.0 * f.K * f.m + 7.0 * f.m + 3.0 * f.K)
+        grad = {"kernel": "srt3d_sketch_grad_step" if pipe.fused else "srt3d_sketch_grad+srt3d_descent_update",
+                "ms_per_iter": per_iter, "pixel_iters_per_s": f.npix / (per_iter * 1e-3),
+                "gbs": g_bytes / (per_iter * 1e-3) / 1e9, "frac_hbm": g_bytes / (per_iter * 1e-3) / 1e9 / hbm,
+                "tflops": g_flops / (per_iter * 1e-3) / 1e12,
+                "frac_fp32": g_flops / (per_iter * 1e-3) / fp32_peak,
+                "note": "per-iteration time includes graph-node launch gaps; z stays L2-resident across iterations"}
+    # dominant kernel -> roofline object
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(f.name, {})
+    if grad is None or sk_avg >= it_avg:
+        roof = {"kernel": "srt3d_sketch", "bound": "alu", "achieved": sketch["tflops"], "peak": fp32_peak / 1e12,
+                "unit": "TFLOP/s", "frac": sketch["frac_fp32"],
+                "peak_source": f"FP32: {nsm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (max clock)",
+                "traffic": (traffic or {}).get("srt3d_sketch")}
+    else:
+        roof = {"kernel": grad["kernel"], "bound": "hbm", "achieved": grad["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": grad["frac_hbm"], "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "traffic": (traffic or {}).get("srt3d_sketch_grad_step")}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        info = oracle_step_sample(f, args.cpu_seconds)
+        cpu = {"value": info["photons"] / info["seconds"], "unit": "photons/s", "cores": info["cores"],
+               "kind": "oracle", "sample": info["sample"]}
+
+    line = {"metric": METRIC, "value": photons_all / (ms_max * 1e-3), "unit": "photons/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Eq. (1) photon frames; stand-in for the paper's head/camouflage datasets)",
+            "config": config_obj(f, args), "clocks": clocks, "e2e": e2e,
+            "gpu_launches": pipe.launches_per_step * args.steps,
+            "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad,
+            "step_definition": "srt3d_sketch over the frame + iters x srt3d_sketch_grad_step (CUDA graphs)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_srt3d(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,156 @@
+/*
+ * srt3d.h — C ABI of libsrt3d.so, the B200 (sm_100a) hot path of sketched
+ * RT3D (SRT3D, arxiv 2203.00952).
+ *
+ * Citations: "PAPER.md:n" = line n of the paper text; readings A1..A17 of
+ * ambiguous passages are listed in DESIGN.md §3.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *    tensors).  The caller owns every buffer; the library allocates no device
+ *    memory and keeps no pointer after the call returns.
+ *  - Calls are asynchronous and stream-ordered: work is enqueued on `stream`
+ *    (a cudaStream_t; NULL = the legacy default stream) and the function
+ *    returns.  Outputs are valid once the stream has synchronised.  Every
+ *    entry point is legal inside CUDA-graph capture, except srt3d_sketch with
+ *    total_photons_hint == 0, which reads two offsets back synchronously.
+ *  - Layouts are row-major.  A sketch / expected sketch is complex64
+ *    interleaved (re, im): float z[npix][m][2] (= torch.complex64 (npix, m)).
+ *    Parameters are float t[npix][K], float alpha[npix][K].
+ *  - Frequencies are the background-blind scheme omega_j = 2*pi*j/T,
+ *    j = 1..m (reading A3).  t is in bins, omega in rad/bin.
+ *  - Return value: SRT3D_OK (0) or a negative error code.  A failing call
+ *    validates everything on the host BEFORE launching, so it writes nothing.
+ *    srt3d_last_error() returns a thread-local message for the last failure.
+ *  - npix == 0 is valid and a no-op.
+ *  - Data preconditions that are NOT checked on the hot path (use
+ *    srt3d_check_csr): 0 <= bins[p] < T, offsets non-decreasing,
+ *    offsets[npix] - offsets[0] < 2^32.  Violations give unspecified values
+ *    but never reads outside bins[offsets[0] .. offsets[npix]).
+ *  - Inputs and outputs must not alias, except that srt3d_descent_update
+ *    updates t and alpha in place.
+ */
+#ifndef SRT3D_H_
+#define SRT3D_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRT3D_OK 0
+#define SRT3D_EINVAL (-1)       /* bad scalar argument (T, m, K, sigma, npix, eta) */
+#define SRT3D_ENULL (-2)        /* required pointer is NULL */
+#define SRT3D_EUNSUPPORTED (-3) /* m > SRT3D_MAX_M or K > SRT3D_MAX_K */
+#define SRT3D_ECUDA (-4)        /* CUDA launch / runtime error (see srt3d_last_error) */
+#define SRT3D_EALIGN (-5)       /* pointer not aligned to its element type */
+
+#define SRT3D_MAX_T 65536u /* bins are uint16 */
+#define SRT3D_MAX_M 64u
+#define SRT3D_MAX_K 8u
+
+/* Library version: major*10000 + minor*100 + patch. */
+int srt3d_version(void);
+
+/* Thread-local message describing the last non-zero return on this thread. */
+const char* srt3d_last_error(void);
+
+/*
+ * srt3d_sketch — Eq. (3), the empirical characteristic
+ * function of each pixel's photon time stamps:
+ *     z[i][j-1] = (1/n_i) * sum_{p in pixel i} exp(i * 2*pi * j * x_p / T),
+ *     j = 1..m,  n_i = offsets[i+1] - offsets[i].
+ * An empty pixel (n_i = 0) gets z = 0 (reading A10).
+ *   bins     uint16 photon bins, pixel-sorted CSR; pixel i owns
+ *            bins[offsets[i] .. offsets[i+1]) (offsets[0] may be non-zero).
+ *            Any 2-byte alignment.
+ *   offsets  uint32 [npix + 1], 4-byte aligned.
+ *   npix     number of pixels (>= 0).
+ *   T        number of time bins, 2 <= T <= 65536.
+ *   m        sketch size, 1 <= m <= min(T - 1, SRT3D_MAX_M).
+ *   z        float [npix][m][2] output, 8-byte aligned; fully overwritten.
+ *   total_photons_hint  offsets[npix] - offsets[0] if the caller knows it
+ *            (selects the launch regime without a device read), else 0.
+ * Arithmetic: the phase index r = (j*x) mod T is exact (integer); phasors
+ * are fp32, accumulated in fp32 in a fixed (deterministic) order.
+ * Errors: SRT3D_EINVAL, SRT3D_ENULL, SRT3D_EUNSUPPORTED, SRT3D_EALIGN,
+ *         SRT3D_ECUDA.
+ */
+int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m,
+                 float* z, uint64_t total_photons_hint, void* stream);
+
+/*
+ * srt3d_expected_sketch — Eq. (4) at omega_j = 2*pi*j/T with
+ * the Gaussian IRF hhat(w) = exp(-sigma^2 w^2 / 2) (BASELINE.json north_star):
+ *     z[i][j-1] = sum_{k<K} alpha[i][k] * hhat(omega_j) * exp(i omega_j t[i][k]).
+ * The background term alpha_0 * CF_uniform(omega_j) is exactly 0 at these
+ * frequencies (reading A4) and is not evaluated.  t may be any
+ * real value (Phi is T-periodic in t; reading A16).
+ *   t, alpha float [npix][K] (4-byte aligned);  K in 1..SRT3D_MAX_K.
+ *   sigma    IRF standard deviation in bins, finite and >= 0.
+ *   z        float [npix][m][2] output (8-byte aligned).
+ */
+int srt3d_expected_sketch(const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
+                          uint32_t m, float* z, void* stream);
+
+/*
+ * srt3d_sketch_grad — the per-pixel sketched data-fidelity term of Eq. (6) /
+ * Eq. (8) with W = I, unweighted by
+ * n (reading A1), and its analytic gradient:
+ *     r_j  = z_j - Phi_j(theta),            Phi_j as in srt3d_expected_sketch
+ *     loss = sum_{j=1..m} |r_j|^2
+ *     grad_alpha[k] = -2 sum_j hhat_j Re( conj(r_j) exp(i omega_j t_k) )
+ *     grad_t[k]     = +2 alpha_k sum_j omega_j hhat_j Im( conj(r_j) exp(i omega_j t_k) )
+ * (d/dalpha_0 = 0 because the background term vanishes at omega_j.)
+ *   z        float [npix][m][2] (8-byte aligned), e.g. the srt3d_sketch output.
+ *   t, alpha float [npix][K].
+ *   grad_t, grad_alpha  float [npix][K] outputs.
+ *   loss     float [npix] output, or NULL to skip it (reading A2: per pixel).
+ */
+int srt3d_sketch_grad(const float* z, const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma,
+                      uint32_t T, uint32_t m, float* grad_t, float* grad_alpha, float* loss, void* stream);
+
+/*
+ * srt3d_descent_update — the harness update step of the pixelwise data step
+ * (reading A13; not an equation of the paper): in place, for every (i, k),
+ *     t     -= clamp(eta * grad_t / (2 max(alpha,0.05)^2 sum_j omega_j^2 hhat_j^2), +-T/(4m)),
+ *              then t is wrapped into [0, T)
+ *     alpha  = clamp(alpha - eta * grad_alpha / (2 sum_j hhat_j^2), 0, 1)
+ * using alpha's value before the update in both lines.
+ *   eta finite and > 0.
+ */
+int srt3d_descent_update(float* t, float* alpha, const float* grad_t, const float* grad_alpha, int64_t npix,
+                         uint32_t K, float sigma, uint32_t T, uint32_t m, float eta, void* stream);
+
+/*
+ * srt3d_sketch_grad_step — srt3d_sketch_grad followed by
+ * srt3d_descent_update in ONE kernel (same arithmetic, grad_t / grad_alpha
+ * never leave registers).  loss may be NULL.  t and alpha are updated in
+ * place; each pixel's reads of t/alpha precede its writes.
+ */
+int srt3d_sketch_grad_step(const float* z, float* t, float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
+                           uint32_t m, float eta, float* loss, void* stream);
+
+/*
+ * srt3d_check_csr — debug validator (not on the hot path).  Sets *bad (a
+ * device int32 the caller zeroes first) to non-zero if some bins[p] >= T or
+ * some offsets[i+1] < offsets[i].
+ */
+int srt3d_check_csr(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, int32_t* bad,
+                    void* stream);
+
+/*
+ * srt3d_debug_phase_index — test export of the exact integer phase index
+ * used by srt3d_sketch: r[p][j-1] = (j * bins[p]) mod T, j = 1..m, computed
+ * by the same device function the sketch kernel uses (PAPER.md:61 with
+ * omega_j = 2 pi j / T).  r is uint32 [n][m].
+ */
+int srt3d_debug_phase_index(const uint16_t* bins, int64_t n, uint32_t T, uint32_t m, uint32_t* r, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRT3D_H_ */

@@ -1,0 +1,198 @@
+"""paper_2203_00952_b200 — B200-native (sm_100a) hot path of sketched RT3D
+(SRT3D, arxiv 2203.00952).
+
+Thin Python binding of ``libsrt3d.so`` (C ABI in ``include/srt3d.h``):
+argument marshalling only.  Every step of the path runs in the CUDA kernels
+behind the ABI; there is no CPU or PyTorch fallback — if the library is
+missing or a call fails, an exception is raised.
+
+Functions take CUDA torch tensors (PyTorch provides device memory and
+streams) and enqueue on the current torch stream unless ``stream`` is given:
+
+  srt3d_sketch(bins, offsets, T, m, z=None)           Eq. (3)
+  srt3d_expected_sketch(t, alpha, sigma, T, m)         Eq. (4)
+  srt3d_sketch_grad(z, t, alpha, sigma, T, m)          Eq. (6)/(8) data term + gradient
+  srt3d_descent_update(t, alpha, gt, ga, sigma, T, m, eta)   harness step (reading A13)
+  srt3d_sketch_grad_step(z, t, alpha, sigma, T, m, eta)      fused grad + update
+  srt3d_check_csr, srt3d_debug_phase_index            validation / test exports
+
+``fit_frame`` / ``fit_frame_host`` run the whole hot path (sketch + N
+gradient iterations) on device-resident or host (pinned) inputs.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsrt3d.so")
+_lib = None
+
+SRT3D_OK = 0
+ERRORS = {-1: "SRT3D_EINVAL", -2: "SRT3D_ENULL", -3: "SRT3D_EUNSUPPORTED", -4: "SRT3D_ECUDA", -5: "SRT3D_EALIGN"}
+EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_expected_sketch", "srt3d_sketch_grad",
+           "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index")
+
+
+class Srt3dError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def load_library(path: str | None = None):
+    """Load libsrt3d.so (raises if it is missing: no fallback path exists)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise ImportError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the CUDA extension is required; there is no CPU fallback)")
+    lib = ctypes.CDLL(p)
+    P, i64, u32, u64, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_float
+    lib.srt3d_version.argtypes = []
+    lib.srt3d_version.restype = ctypes.c_int
+    lib.srt3d_last_error.argtypes = []
+    lib.srt3d_last_error.restype = ctypes.c_char_p
+    lib.srt3d_sketch.argtypes = [P, P, i64, u32, u32, P, u64, P]
+    lib.srt3d_expected_sketch.argtypes = [P, P, i64, u32, f32, u32, u32, P, P]
+    lib.srt3d_sketch_grad.argtypes = [P, P, P, i64, u32, f32, u32, u32, P, P, P, P]
+    lib.srt3d_descent_update.argtypes = [P, P, P, P, i64, u32, f32, u32, u32, f32, P]
+    lib.srt3d_sketch_grad_step.argtypes = [P, P, P, i64, u32, f32, u32, u32, f32, P, P]
+    lib.srt3d_check_csr.argtypes = [P, P, i64, u32, P, P]
+    lib.srt3d_debug_phase_index.argtypes = [P, i64, u32, u32, P, P]
+    for f in EXPORTS[2:]:
+        getattr(lib, f).restype = ctypes.c_int
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _call(fn_name: str, *args):
+    lib = load_library()
+    rc = getattr(lib, fn_name)(*args)
+    if rc != SRT3D_OK:
+        raise Srt3dError(rc, lib.srt3d_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("all tensors must be contiguous CUDA tensors")
+
+
+def srt3d_sketch(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: torch.Tensor | None = None,
+                 total_photons: int | None = None, stream=None) -> torch.Tensor:
+    """Eq. (3): complex64 (npix, m) sketch of a uint16/uint32 CSR frame on the GPU."""
+    npix = offsets.numel() - 1
+    if z is None:
+        z = torch.empty((max(npix, 0), m), dtype=torch.complex64, device=offsets.device)
+    _need_cuda(bins, offsets, z)
+    assert bins.dtype == torch.uint16 and offsets.dtype == torch.uint32 and z.dtype == torch.complex64
+    hint = int(total_photons) if total_photons is not None else 0
+    _call("srt3d_sketch", _ptr(bins), _ptr(offsets), npix, T, m, _ptr(z), hint, _stream(stream))
+    return z
+
+
+def srt3d_expected_sketch(t: torch.Tensor, alpha: torch.Tensor, sigma: float, T: int, m: int,
+                          z: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Eq. (4) with Gaussian hhat: complex64 (npix, m)."""
+    npix, K = t.shape
+    if z is None:
+        z = torch.empty((npix, m), dtype=torch.complex64, device=t.device)
+    _need_cuda(t, alpha, z)
+    _call("srt3d_expected_sketch", _ptr(t), _ptr(alpha), npix, K, float(sigma), T, m, _ptr(z), _stream(stream))
+    return z
+
+
+def srt3d_sketch_grad(z: torch.Tensor, t: torch.Tensor, alpha: torch.Tensor, sigma: float, T: int, m: int,
+                      grad_t=None, grad_alpha=None, loss=None, want_loss: bool = True, stream=None):
+    """Sketched loss ||z - Phi(theta)||^2 per pixel and its gradient (grad_t, grad_alpha, loss)."""
+    npix, K = t.shape
+    if grad_t is None:
+        grad_t = torch.empty_like(t)
+    if grad_alpha is None:
+        grad_alpha = torch.empty_like(alpha)
+    if loss is None and want_loss:
+        loss = torch.empty(npix, dtype=torch.float32, device=t.device)
+    _need_cuda(z, t, alpha, grad_t, grad_alpha, loss)
+    _call("srt3d_sketch_grad", _ptr(z), _ptr(t), _ptr(alpha), npix, K, float(sigma), T, m, _ptr(grad_t),
+          _ptr(grad_alpha), _ptr(loss), _stream(stream))
+    return grad_t, grad_alpha, loss
+
+
+def srt3d_descent_update(t, alpha, grad_t, grad_alpha, sigma: float, T: int, m: int, eta: float = 0.5, stream=None):
+    """In-place harness update of (t, alpha) (reading A13)."""
+    npix, K = t.shape
+    _need_cuda(t, alpha, grad_t, grad_alpha)
+    _call("srt3d_descent_update", _ptr(t), _ptr(alpha), _ptr(grad_t), _ptr(grad_alpha), npix, K, float(sigma), T, m,
+          float(eta), _stream(stream))
+    return t, alpha
+
+
+def srt3d_sketch_grad_step(z, t, alpha, sigma: float, T: int, m: int, eta: float = 0.5, loss=None, stream=None):
+    """Fused gradient + in-place update of (t, alpha); optional per-pixel loss."""
+    npix, K = t.shape
+    _need_cuda(z, t, alpha, loss)
+    _call("srt3d_sketch_grad_step", _ptr(z), _ptr(t), _ptr(alpha), npix, K, float(sigma), T, m, float(eta),
+          _ptr(loss), _stream(stream))
+    return t, alpha
+
+
+def srt3d_check_csr(bins, offsets, T: int, stream=None) -> int:
+    npix = offsets.numel() - 1
+    bad = torch.zeros(1, dtype=torch.int32, device=offsets.device)
+    _need_cuda(bins, offsets)
+    _call("srt3d_check_csr", _ptr(bins), _ptr(offsets), npix, T, _ptr(bad), _stream(stream))
+    return int(bad.item())
+
+
+def srt3d_debug_phase_index(bins, T: int, m: int, stream=None) -> torch.Tensor:
+    n = bins.numel()
+    r = torch.empty((n, m), dtype=torch.uint32, device=bins.device)
+    _need_cuda(bins, r)
+    _call("srt3d_debug_phase_index", _ptr(bins), n, T, m, _ptr(r), _stream(stream))
+    return r
+
+
+def fit_frame(bins, offsets, t0, alpha0, sigma: float, T: int, m: int, iters: int, eta: float = 0.5,
+              total_photons: int | None = None, fused: bool = False, z=None, t=None, alpha=None, gt=None, ga=None,
+              stream=None):
+    """The whole hot path on device-resident inputs: sketch the frame (Eq. 3),
+    then ``iters`` sketched-gradient iterations (Eq. 6/8 data step) from
+    (t0, alpha0).  Returns (z, t, alpha)."""
+    z = srt3d_sketch(bins, offsets, T, m, z=z, total_photons=total_photons, stream=stream)
+    if t is None:
+        t = t0.clone()
+        alpha = alpha0.clone()
+    else:
+        t.copy_(t0)
+        alpha.copy_(alpha0)
+    if not fused:
+        if gt is None:
+            gt = torch.empty_like(t)
+            ga = torch.empty_like(alpha)
+    for _ in range(iters):
+        if fused:
+            srt3d_sketch_grad_step(z, t, alpha, sigma, T, m, eta, stream=stream)
+        else:
+            srt3d_sketch_grad(z, t, alpha, sigma, T, m, grad_t=gt, grad_alpha=ga, want_loss=False, stream=stream)
+            srt3d_descent_update(t, alpha, gt, ga, sigma, T, m, eta, stream=stream)
+    return z, t, alpha
+
+
+def version() -> int:
+    return int(load_library().srt3d_version())

@@ -1,0 +1,254 @@
+// C ABI of libsrt3d.so (declared in include/srt3d.h): host-side validation,
+// per-call constants (fp64 on the host), launch-regime choice and error
+// reporting.  Validation precedes every launch, so a failing call writes
+// nothing.
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../include/srt3d.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "no error";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SRT3D_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+int num_sms_current() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+int check_tm(uint32_t T, uint32_t m) {
+  if (T < 2 || T > SRT3D_MAX_T) return fail(SRT3D_EINVAL, "T=%u out of range [2, %u]", T, SRT3D_MAX_T);
+  if (m < 1 || m >= T) return fail(SRT3D_EINVAL, "m=%u must satisfy 1 <= m <= T-1 (T=%u)", m, T);
+  if (m > SRT3D_MAX_M) return fail(SRT3D_EUNSUPPORTED, "m=%u exceeds SRT3D_MAX_M=%u", m, SRT3D_MAX_M);
+  return SRT3D_OK;
+}
+
+int check_kparams(int64_t npix, uint32_t K, float sigma, uint32_t T, uint32_t m) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  int rc = check_tm(T, m);
+  if (rc) return rc;
+  if (K < 1) return fail(SRT3D_EINVAL, "K=%u < 1", K);
+  if (K > SRT3D_MAX_K) return fail(SRT3D_EUNSUPPORTED, "K=%u exceeds SRT3D_MAX_K=%u", K, SRT3D_MAX_K);
+  if (!std::isfinite(sigma) || sigma < 0.f) return fail(SRT3D_EINVAL, "sigma=%g must be finite and >= 0", (double)sigma);
+  return SRT3D_OK;
+}
+
+// fp64 constants, rounded once
+void fill_consts(srt3d::PixArgs& a, float sigma, uint32_t T, uint32_t m, float eta) {
+  const double pi = 3.14159265358979323846;
+  double sw2h2 = 0.0, sh2 = 0.0;
+  for (int j = 0; j < srt3d::MAX_M; j++) {
+    a.c.hh[j] = 0.f;
+    a.c.wh[j] = 0.f;
+  }
+  for (uint32_t j = 1; j <= m; j++) {
+    const double w = 2.0 * pi * (double)j / (double)T;
+    const double h = std::exp(-(double)sigma * (double)sigma * w * w / 2.0);
+    a.c.hh[j - 1] = (float)h;
+    a.c.wh[j - 1] = (float)(w * h);
+    sw2h2 += w * w * h * h;
+    sh2 += h * h;
+  }
+  a.T = T;
+  a.m = m;
+  a.invT = 1.0 / (double)T;
+  a.Tf = (float)T;
+  a.eta = eta;
+  a.upd_t_scale = (float)(1.0 / (2.0 * sw2h2));
+  a.upd_a_scale = (float)(1.0 / (2.0 * sh2));
+  a.max_step = (float)((double)T / (4.0 * (double)m));
+}
+
+int lanes_for(double mean_photons) {
+  // >= ~32 photons per lane amortises the group reduce-scatter
+  if (mean_photons >= 1024.0) return 32;
+  if (mean_photons >= 512.0) return 16;
+  if (mean_photons >= 256.0) return 8;
+  return 4;
+}
+
+}  // namespace
+
+extern "C" {
+
+int srt3d_version(void) { return 100; }
+
+const char* srt3d_last_error(void) { return g_err; }
+
+int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
+                 uint64_t total_photons_hint, void* stream) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  int rc = check_tm(T, m);
+  if (rc) return rc;
+  if (npix == 0) return SRT3D_OK;
+  if (!offsets || !z) return fail(SRT3D_ENULL, "offsets/z must be non-NULL");
+  if (!bins && total_photons_hint != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
+  if (!aligned(bins, 2) || !aligned(offsets, 4) || !aligned(z, 8))
+    return fail(SRT3D_EALIGN, "bins/offsets/z must be 2/4/8-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t total = total_photons_hint;
+  if (total == 0) {
+    uint32_t ends[2] = {0, 0};
+    cudaError_t e = cudaMemcpyAsync(&ends[0], offsets, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&ends[1], offsets + npix, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch(read offsets)");
+    total = ends[1] >= ends[0] ? (uint64_t)(ends[1] - ends[0]) : 0;
+  }
+  if (!bins && total != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
+  const int G = lanes_for((double)total / (double)npix);
+  const int nsm = num_sms_current();
+  srt3d::SketchArgs a;
+  a.bins = bins ? bins : reinterpret_cast<const uint16_t*>(offsets);  // never dereferenced when no photons
+  a.offsets = offsets;
+  a.npix = npix;
+  a.T = T;
+  a.mstride = m;
+  a.z = z;
+  for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+    a.j0 = j0;
+    const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
+    cudaError_t e = srt3d::launch_sketch_pass(M, G, a, s, nsm);
+    if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
+  }
+  return SRT3D_OK;
+}
+
+int srt3d_expected_sketch(const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
+                          uint32_t m, float* z, void* stream) {
+  int rc = check_kparams(npix, K, sigma, T, m);
+  if (rc) return rc;
+  if (npix == 0) return SRT3D_OK;
+  if (!t || !alpha || !z) return fail(SRT3D_ENULL, "t/alpha/z must be non-NULL");
+  if (!aligned(t, 4) || !aligned(alpha, 4) || !aligned(z, 8))
+    return fail(SRT3D_EALIGN, "t/alpha must be 4-byte and z 8-byte aligned");
+  srt3d::PixArgs a = {};
+  fill_consts(a, sigma, T, m, 0.f);
+  a.t_in = t;
+  a.a_in = alpha;
+  a.zout = z;
+  a.npix = npix;
+  cudaError_t e = srt3d::launch_pixel(srt3d::PX_EXPECTED, (int)K, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_expected_sketch");
+  return SRT3D_OK;
+}
+
+int srt3d_sketch_grad(const float* z, const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma,
+                      uint32_t T, uint32_t m, float* grad_t, float* grad_alpha, float* loss, void* stream) {
+  int rc = check_kparams(npix, K, sigma, T, m);
+  if (rc) return rc;
+  if (npix == 0) return SRT3D_OK;
+  if (!z || !t || !alpha || !grad_t || !grad_alpha) return fail(SRT3D_ENULL, "z/t/alpha/grad_t/grad_alpha must be non-NULL");
+  if (!aligned(z, 8) || !aligned(t, 4) || !aligned(alpha, 4) || !aligned(grad_t, 4) || !aligned(grad_alpha, 4) ||
+      (loss && !aligned(loss, 4)))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and t/alpha/grads/loss 4-byte aligned");
+  srt3d::PixArgs a = {};
+  fill_consts(a, sigma, T, m, 0.f);
+  a.z = z;
+  a.t_in = t;
+  a.a_in = alpha;
+  a.grad_t = grad_t;
+  a.grad_a = grad_alpha;
+  a.loss = loss;
+  a.npix = npix;
+  cudaError_t e = srt3d::launch_pixel(srt3d::PX_GRAD, (int)K, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch_grad");
+  return SRT3D_OK;
+}
+
+int srt3d_descent_update(float* t, float* alpha, const float* grad_t, const float* grad_alpha, int64_t npix,
+                         uint32_t K, float sigma, uint32_t T, uint32_t m, float eta, void* stream) {
+  int rc = check_kparams(npix, K, sigma, T, m);
+  if (rc) return rc;
+  if (!std::isfinite(eta) || eta <= 0.f) return fail(SRT3D_EINVAL, "eta=%g must be finite and > 0", (double)eta);
+  if (npix == 0) return SRT3D_OK;
+  if (!t || !alpha || !grad_t || !grad_alpha) return fail(SRT3D_ENULL, "t/alpha/grad_t/grad_alpha must be non-NULL");
+  if (!aligned(t, 4) || !aligned(alpha, 4) || !aligned(grad_t, 4) || !aligned(grad_alpha, 4))
+    return fail(SRT3D_EALIGN, "t/alpha/grads must be 4-byte aligned");
+  srt3d::PixArgs a = {};
+  fill_consts(a, sigma, T, m, eta);
+  a.t_in = t;
+  a.a_in = alpha;
+  a.t_out = t;
+  a.a_out = alpha;
+  a.grad_t = const_cast<float*>(grad_t);
+  a.grad_a = const_cast<float*>(grad_alpha);
+  a.npix = npix;
+  cudaError_t e = srt3d::launch_pixel(srt3d::PX_UPDATE, (int)K, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_descent_update");
+  return SRT3D_OK;
+}
+
+int srt3d_sketch_grad_step(const float* z, float* t, float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
+                           uint32_t m, float eta, float* loss, void* stream) {
+  int rc = check_kparams(npix, K, sigma, T, m);
+  if (rc) return rc;
+  if (!std::isfinite(eta) || eta <= 0.f) return fail(SRT3D_EINVAL, "eta=%g must be finite and > 0", (double)eta);
+  if (npix == 0) return SRT3D_OK;
+  if (!z || !t || !alpha) return fail(SRT3D_ENULL, "z/t/alpha must be non-NULL");
+  if (!aligned(z, 8) || !aligned(t, 4) || !aligned(alpha, 4) || (loss && !aligned(loss, 4)))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and t/alpha/loss 4-byte aligned");
+  srt3d::PixArgs a = {};
+  fill_consts(a, sigma, T, m, eta);
+  a.z = z;
+  a.t_in = t;
+  a.a_in = alpha;
+  a.t_out = t;
+  a.a_out = alpha;
+  a.loss = loss;
+  a.npix = npix;
+  cudaError_t e = srt3d::launch_pixel(srt3d::PX_GRAD_STEP, (int)K, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch_grad_step");
+  return SRT3D_OK;
+}
+
+int srt3d_check_csr(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, int32_t* bad,
+                    void* stream) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  if (T < 2 || T > SRT3D_MAX_T) return fail(SRT3D_EINVAL, "T=%u out of range", T);
+  if (npix == 0) return SRT3D_OK;
+  if (!bins || !offsets || !bad) return fail(SRT3D_ENULL, "bins/offsets/bad must be non-NULL");
+  cudaError_t e = srt3d::launch_check_csr(bins, offsets, npix, T, bad, (cudaStream_t)stream, num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_check_csr");
+  return SRT3D_OK;
+}
+
+int srt3d_debug_phase_index(const uint16_t* bins, int64_t n, uint32_t T, uint32_t m, uint32_t* r, void* stream) {
+  if (n < 0) return fail(SRT3D_EINVAL, "n=%lld < 0", (long long)n);
+  if (T < 2 || T > SRT3D_MAX_T) return fail(SRT3D_EINVAL, "T=%u out of range", T);
+  if (m < 1 || m > SRT3D_MAX_M) return fail(SRT3D_EINVAL, "m=%u out of range", m);
+  if (n == 0) return SRT3D_OK;
+  if (!bins || !r) return fail(SRT3D_ENULL, "bins/r must be non-NULL");
+  if (!aligned(r, 4)) return fail(SRT3D_EALIGN, "r must be 4-byte aligned");
+  cudaError_t e = srt3d::launch_phase_index(bins, n, T, m, r, (cudaStream_t)stream, num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_debug_phase_index");
+  return SRT3D_OK;
+}
+
+}  // extern "C"

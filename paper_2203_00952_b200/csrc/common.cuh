@@ -1,0 +1,75 @@
+// Shared device helpers for the SRT3D sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace srt3d {
+
+typedef unsigned long long u64;
+
+// ---- packed fp32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2) -------------
+// A u64 holds (lo, hi) = (re, im).  ptxas folds the scalar broadcasts built
+// with pk(s, s) into the .F32 operand form, so no MOVs are emitted.
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo_of(u64 v) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi_of(u64 v) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 fmul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// Complex multiply p * w with packed ops: (pr,pr)*(wr,wi) + (pi,pi)*(-wi,wr).
+// W = (wr, wi), Wn = (-wi, wr).  2 instructions, 4 FP32 lane-ops.
+__device__ __forceinline__ u64 cmul2(u64 p, u64 W, u64 Wn) {
+  return ffma2(pk(hi_of(p), hi_of(p)), Wn, fmul2(pk(lo_of(p), lo_of(p)), W));
+}
+
+// ---- exact integer phase index (PAPER.md:61 with omega_j = 2 pi j / T) -----
+// r = (j * x) mod T for x < T <= 65536, j <= 64: j*x < 2^22, exact in uint32.
+__device__ __forceinline__ uint32_t phase_index(uint32_t x, uint32_t j, uint32_t T) {
+  return (j * x) % T;
+}
+
+// ---- fixed-point phase of a real depth (expected sketch / gradient) --------
+// q = round(frac(t / T) * 2^32) as uint32: t/T in revolutions, 32-bit fixed
+// point.  j*q (mod 2^32) is then the exact phase of omega_j * t up to the
+// 2^-33 revolution quantisation of q, for any j (no fp32 range-reduction
+// error even when j*t is large).
+__device__ __forceinline__ uint32_t phase_q32(float t, double invT) {
+  double r = (double)t * invT;  // revolutions, relative error ~1e-16
+  r -= floor(r);                // frac in [0, 1)
+  return (uint32_t)(unsigned long long)__double2ll_rn(r * 4294967296.0);  // 2^32 wraps to 0
+}
+// exp(i * 2 pi * q / 2^32) with q interpreted as a signed half-open
+// revolution in [-1/2, 1/2): sincospif on a = q * 2^-31 in [-1, 1).
+__device__ __forceinline__ float2 phasor_q32(uint32_t q) {
+  float a = (float)(int32_t)q * 4.656612873077392578125e-10f;  // 2^-31
+  float s, c;
+  sincospif(a, &s, &c);
+  return make_float2(c, s);
+}
+
+}  // namespace srt3d

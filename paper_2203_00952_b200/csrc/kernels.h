@@ -1,0 +1,62 @@
+// Internal declarations shared by the kernel translation units and the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace srt3d {
+
+constexpr int SK_THREADS = 256;                 // sketch CTA size
+constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T <= 24576 uses the smem table)
+constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
+constexpr int MAX_M = 64;
+constexpr int MAX_K = 8;
+
+struct SketchArgs {
+  const uint16_t* bins;
+  const uint32_t* offsets;
+  long long npix;
+  uint32_t T;
+  uint32_t j0;       // first frequency of this pass is j0 + 1
+  uint32_t mstride;  // m of the output row
+  float* z;
+};
+
+// Per-call frequency constants, computed on the host in fp64 and rounded:
+// hh[j-1] = hhat(omega_j) = exp(-sigma^2 omega_j^2 / 2), wh[j-1] = omega_j * hhat(omega_j).
+struct FreqConsts {
+  float hh[MAX_M];
+  float wh[MAX_M];
+};
+
+struct PixArgs {
+  const float* z;     // [npix][m][2] (grad) or output (expected sketch)
+  float* zout;
+  const float* t_in;
+  const float* a_in;
+  float* t_out;       // update modes
+  float* a_out;
+  float* grad_t;
+  float* grad_a;
+  float* loss;
+  long long npix;
+  uint32_t T;
+  uint32_t m;
+  double invT;
+  float eta;
+  float upd_t_scale;  // 1 / (2 * sum_j omega_j^2 hhat_j^2)
+  float upd_a_scale;  // 1 / (2 * sum_j hhat_j^2)
+  float max_step;     // T / (4 m)
+  float Tf;
+  FreqConsts c;
+};
+
+enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3 };
+
+cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms);
+cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, uint32_t m, uint32_t* r,
+                               cudaStream_t s, int num_sms);
+cudaError_t launch_check_csr(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,
+                             int32_t* bad, cudaStream_t s, int num_sms);
+cudaError_t launch_pixel(PixMode mode, int K, const PixArgs& a, cudaStream_t s);
+
+}  // namespace srt3d

@@ -1,0 +1,8 @@
+// K1 instantiations for G = 8 lanes per pixel (split for parallel builds).
+#include "sketch_impl.cuh"
+
+namespace srt3d {
+cudaError_t launch_sketch_g8(int M, bool tab, const SketchArgs& a, cudaStream_t s, int num_sms) {
+  return dispatch_m<8, true>(M, a, s, num_sms);
+}
+}  // namespace srt3d

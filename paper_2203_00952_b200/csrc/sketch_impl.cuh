@@ -1,0 +1,260 @@
+#pragma once
+// K1 — photon -> sketch accumulator, Eq. (3) on sm_100a.
+//
+//   z[i][j-1] = (1/n_i) sum_p exp(i 2 pi j x_p / T),  j = j0+1 .. j0+M
+//
+// Design:
+//  * Each CTA first fills a shared-memory table tab[r] = exp(i 2 pi r / T),
+//    r < T, rounded to fp32 from fp64 sincospi (exact-index phasors; the
+//    index r = (j x) mod T is integer-exact).  The CTA is persistent and
+//    reuses the table for every pixel it visits.
+//  * A pixel is owned by a group of G lanes (G = 4, 8, 16 or 32; chosen from
+//    the mean photons per pixel).  Photons are read as 16-byte vectors (8
+//    uint16 bins per lane per load, coalesced across the group), after a
+//    scalar head/tail peel that aligns the pixel's segment.
+//  * Per photon x: w = tab[x], then the complex-power recurrence
+//    p_j = p_{j-1} * w on the packed FP32x2 pipe (FMUL2 + FFMA2 per term) and
+//    S_j += p_j (FADD2): 3 instructions / 6 FP32 lane-ops per (photon, j).
+//    The worst-case fp32 drift over 32 steps from the exact w is 1.4e-6
+//    (tools/sim_phasor_error.py), so no re-anchoring is needed for M <= 32;
+//    m > 32 runs a second pass anchored at tab[(33 x) mod T].
+//  * Accumulation is bounded: every super-chunk of <= 128 photons per lane is
+//    folded across the group with a shuffle butterfly reduce-scatter (each
+//    lane keeps 2M/G sums) into per-lane fp32 results.  The order is fixed,
+//    so results are bitwise reproducible.
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace srt3d {
+
+// exp(i 2 pi r / T) for r < T into shared memory, fp64 sincospi on the
+// centred index so the argument stays in (-1, 1].
+__device__ __forceinline__ void build_phase_table(float2* tab, uint32_t T) {
+  const double s = 2.0 / (double)T;
+  for (uint32_t r = threadIdx.x; r < T; r += blockDim.x) {
+    int rc = (2u * r > T) ? (int)r - (int)T : (int)r;
+    double sn, cs;
+    sincospi(s * (double)rc, &sn, &cs);
+    tab[r] = make_float2((float)cs, (float)sn);
+  }
+}
+
+// Exact phasor without a table (T too large for shared memory): fp64.
+__device__ __forceinline__ float2 phasor_exact(uint32_t r, uint32_t T) {
+  int rc = (2u * r > T) ? (int)r - (int)T : (int)r;
+  double sn, cs;
+  sincospi(2.0 * (double)rc / (double)T, &sn, &cs);
+  return make_float2((float)cs, (float)sn);
+}
+
+template <int M, bool TAB>
+struct PhotonAcc {
+  u64 acc[M];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int j = 0; j < M; j++) acc[j] = 0ull;
+  }
+  __device__ __forceinline__ float2 base(const float2* tab, uint32_t r, uint32_t T) const {
+    if (TAB) return tab[r];
+    return phasor_exact(r, T);
+  }
+  // one photon
+  __device__ __forceinline__ void add1(const float2* tab, uint32_t x, uint32_t T, uint32_t j0) {
+    float2 w = base(tab, x, T);
+    u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
+    u64 P = W;
+    if (j0) {
+      float2 a = base(tab, phase_index(x, j0 + 1, T), T);
+      P = pk(a.x, a.y);
+    }
+    acc[0] = fadd2(acc[0], P);
+#pragma unroll
+    for (int j = 1; j < M; j++) {
+      P = cmul2(P, W, Wn);
+      acc[j] = fadd2(acc[j], P);
+    }
+  }
+  // two photons, interleaved chains (ILP 2)
+  __device__ __forceinline__ void add2(const float2* tab, uint32_t x, uint32_t y, uint32_t T, uint32_t j0) {
+    float2 w = base(tab, x, T), v = base(tab, y, T);
+    u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
+    u64 V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
+    u64 P = W, Q = V;
+    if (j0) {
+      float2 a = base(tab, phase_index(x, j0 + 1, T), T);
+      float2 b = base(tab, phase_index(y, j0 + 1, T), T);
+      P = pk(a.x, a.y);
+      Q = pk(b.x, b.y);
+    }
+    acc[0] = fadd2(acc[0], fadd2(P, Q));
+#pragma unroll
+    for (int j = 1; j < M; j++) {
+      P = cmul2(P, W, Wn);
+      Q = cmul2(Q, V, Vn);
+      acc[j] = fadd2(acc[j], fadd2(P, Q));
+    }
+  }
+};
+
+// Butterfly reduce-scatter of NV floats over the G lanes of a group.  On
+// return v[0 .. NV/G) of lane gl holds the group sums of the original
+// entries [gl*NV/G, (gl+1)*NV/G).  Fixed order => deterministic.
+template <int NV, int G>
+__device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int gl) {
+#pragma unroll
+  for (int d = G / 2, n = NV; d >= 1; d >>= 1, n >>= 1) {
+    const bool up = (gl & d) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; i++) {
+      float send = up ? v[i] : v[i + n / 2];
+      float keep = up ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, d);
+    }
+  }
+}
+
+template <int M, int G, bool TAB>
+__global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
+  extern __shared__ float2 tab[];
+  if (TAB) {
+    build_phase_table(tab, a.T);
+    __syncthreads();
+  }
+  constexpr int PPW = 32 / G;                    // pixels per warp
+  constexpr int NV = 2 * M;                      // floats per pixel
+  constexpr int NVP = ((NV + G - 1) / G) * G;    // padded to a multiple of G
+  constexpr int VL = NVP / G;                    // floats per lane after reduce-scatter
+  constexpr int CPL = 16;                        // 16B chunks per lane per super-chunk (128 photons)
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const long long warp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long ntiles = (a.npix + PPW - 1) / PPW;
+  // bins pointer is 2-byte aligned; slot s = p + off0 is 16-byte aligned when s % 8 == 0
+  const uint32_t off0 = (uint32_t)(((uintptr_t)a.bins >> 1) & 7u);
+  const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(a.bins - off0);
+  const uint16_t* __restrict__ bins = a.bins;
+  const uint32_t T = a.T, j0 = a.j0;
+
+  for (long long tile = warp0; tile < ntiles; tile += nwarps) {
+    const long long pix = tile * PPW + grp;
+    const bool valid = pix < a.npix;
+    unsigned long long beg = 0, end = 0;
+    if (valid) {
+      beg = a.offsets[pix];
+      end = a.offsets[pix + 1];
+      if (end < beg) end = beg;  // malformed CSR: treat as empty (never read out of range)
+    }
+    // aligned body in slot space (slot = photon index + off0; 16B aligned when % 8 == 0)
+    const unsigned long long asb = (beg + off0 + 7u) & ~7ull;
+    const unsigned long long ase = (end + off0) & ~7ull;
+    unsigned long long hend = end, tbeg = end;
+    long long cb = 0, ce = 0;
+    if (asb < ase) {
+      hend = asb - off0;
+      tbeg = ase - off0;
+      cb = (long long)(asb >> 3);
+      ce = (long long)(ase >> 3);
+    }
+    PhotonAcc<M, TAB> pa;
+    pa.zero();
+    // scalar head and tail peel (< 8 photons each)
+    for (unsigned long long p = beg + gl; p < hend; p += G) pa.add1(tab, bins[p], T, j0);
+    for (unsigned long long p = tbeg + gl; p < end; p += G) pa.add1(tab, bins[p], T, j0);
+
+    // warp-uniform number of super-chunks
+    const long long nchunks = ce - cb;
+    int nsc = (int)((nchunks + (long long)G * CPL - 1) / ((long long)G * CPL));
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) nsc = max(nsc, __shfl_xor_sync(0xffffffffu, nsc, d));
+    if (nsc == 0) nsc = 1;
+
+    float res[VL];
+#pragma unroll
+    for (int i = 0; i < VL; i++) res[i] = 0.f;
+
+    for (int sc = 0; sc < nsc; sc++) {
+      const long long c0 = cb + (long long)sc * G * CPL;
+#pragma unroll 2
+      for (int k = 0; k < CPL; k++) {
+        const long long c = c0 + gl + (long long)k * G;
+        if (c < ce) {
+          uint4 v = __ldg(vb + c);
+          pa.add2(tab, v.x & 0xffffu, v.x >> 16, T, j0);
+          pa.add2(tab, v.y & 0xffffu, v.y >> 16, T, j0);
+          pa.add2(tab, v.z & 0xffffu, v.z >> 16, T, j0);
+          pa.add2(tab, v.w & 0xffffu, v.w >> 16, T, j0);
+        }
+      }
+      float f[NVP];
+#pragma unroll
+      for (int j = 0; j < M; j++) {
+        f[2 * j] = lo_of(pa.acc[j]);
+        f[2 * j + 1] = hi_of(pa.acc[j]);
+      }
+#pragma unroll
+      for (int i = NV; i < NVP; i++) f[i] = 0.f;
+      group_reduce_scatter<NVP, G>(f, gl);
+#pragma unroll
+      for (int i = 0; i < VL; i++) res[i] += f[i];
+      pa.zero();
+    }
+    if (valid) {
+      const unsigned long long n = end - beg;
+      const float inv = n ? 1.0f / (float)n : 0.0f;
+      float* zrow = a.z + ((size_t)pix * a.mstride + j0) * 2;
+#pragma unroll
+      for (int i = 0; i < VL; i++) {
+        const int idx = gl * VL + i;
+        if (idx < NV) zrow[idx] = res[i] * inv;
+      }
+    }
+  }
+}
+
+// ---- host-side dispatch ---------------------------------------------------
+template <int M, int G, bool TAB>
+static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
+  auto fn = sketch_kernel<M, G, TAB>;
+  const size_t smem = TAB ? sizeof(float2) * a.T : 0;
+  static bool attr_set = false;  // benign race: idempotent attribute set
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_MAX_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SK_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  constexpr int PPW = 32 / G;
+  const long long tiles = (a.npix + PPW - 1) / PPW;
+  const long long need = (tiles + (SK_THREADS / 32) - 1) / (SK_THREADS / 32);
+  long long grid = (long long)per_sm * num_sms;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  fn<<<(unsigned)grid, SK_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int G, bool TAB>
+static cudaError_t dispatch_m(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
+  switch (M) {
+#define SRT3D_CASE(MM) \
+  case MM:             \
+    return launch_sketch_t<MM, G, TAB>(a, s, num_sms);
+    SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
+    SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
+    SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)
+    SRT3D_CASE(23) SRT3D_CASE(24) SRT3D_CASE(25) SRT3D_CASE(26) SRT3D_CASE(27) SRT3D_CASE(28) SRT3D_CASE(29)
+    SRT3D_CASE(30) SRT3D_CASE(31) SRT3D_CASE(32)
+#undef SRT3D_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace srt3d

@@ -1,0 +1,338 @@
+"""GPU <-> oracle parity through the C ABI (libsrt3d.so), element by element on
+the same seeded inputs.
+
+Tolerances:
+  * integer phase index: bit-exact (==)
+  * sketch / expected sketch: |delta| <= 1e-5 absolute per component (BASELINE north_star)
+  * loss / gradients: |delta| <= 1e-4 |ref| + 1e-5 * S per component, where S is the sum of
+    absolute terms of that component (reading A12; the floor is 5x the worst-case fp32
+    phasor error bound 2e-6 * S), plus frame-level ||delta||_2 / ||ref||_2 <= 1e-4.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SKETCH_ATOL = 1e-5
+
+
+def _dev(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def _csr(lists):
+    offs = np.zeros(len(lists) + 1, dtype=np.uint32)
+    offs[1:] = np.cumsum([len(l) for l in lists])
+    bins = np.concatenate([np.asarray(l, dtype=np.uint16) for l in lists]) if offs[-1] else np.zeros(0, np.uint16)
+    return bins, offs
+
+
+def _sub_csr(bins, offsets, idx):
+    """Photon lists of the pixels idx as a fresh CSR (for sampled oracle checks)."""
+    lists = [bins[offsets[i]:offsets[i + 1]] for i in idx]
+    return _csr(lists)
+
+
+def _gpu_sketch(gpu, bins, offs, T, m, hint=True):
+    import torch
+
+    z = gpu.srt3d_sketch(_dev(bins) if bins.size else torch.zeros(1, dtype=torch.uint16, device="cuda"),
+                         _dev(offs), T, m, total_photons=int(offs[-1] - offs[0]) if hint else None)
+    torch.cuda.synchronize()
+    return _host(z)
+
+
+def _assert_sketch_close(zg, zo, atol=SKETCH_ATOL):
+    d = max(np.abs(zg.real - zo.real).max(initial=0), np.abs(zg.imag - zo.imag).max(initial=0))
+    assert d <= atol, f"max |delta| = {d:.3e} > {atol}"
+    return d
+
+
+# ------------------------------------------------------------ phase index (B1)
+def test_phase_index_bit_exact(gpu, oracle_mod):
+    rng = np.random.default_rng(0)
+    for T, m in [(1024, 4), (4613, 10), (2500, 20), (4096, 10), (8192, 32), (65535, 64), (65536, 64), (2, 1),
+                 (3, 2), (17, 16)]:
+        x = rng.integers(0, T, 5000).astype(np.uint16)
+        x[:3] = [0, T - 1, T // 2]
+        r = _host(gpu.srt3d_debug_phase_index(_dev(x), T, m))
+        ro = oracle_mod.phase_index(x, T, m)
+        assert r.dtype == np.uint32 and np.array_equal(r, ro), (T, m)
+
+
+# ------------------------------------------------------------------ sketch K1
+@pytest.mark.parametrize("T,m", [(1024, 4), (4613, 10), (2500, 20), (4096, 10), (8192, 32), (8192, 64),
+                                 (100, 1), (17, 16), (3, 2), (2, 1), (65536, 64), (40000, 33)])
+@pytest.mark.parametrize("max_n", [9, 300, 3000])
+def test_sketch_ragged_parity(gpu, oracle_mod, inputs_mod, T, m, max_n):
+    """Ragged frames with empty pixels; several tiles and a ragged tail; all lane-group regimes."""
+    bins, offs = inputs_mod.random_csr(npix=777, T=T, max_n=max_n, seed=T * 7 + m + max_n)
+    zg = _gpu_sketch(gpu, bins, offs, T, m)
+    zo = oracle_mod.sketch(bins, offs, T, m)
+    _assert_sketch_close(zg, zo)
+    assert np.all(zg[np.diff(offs.astype(np.int64)) == 0] == 0)
+
+
+def test_sketch_regimes_by_hint(gpu, oracle_mod, inputs_mod):
+    """Every lane-group size (hint-selected) gives the same parity on the same frame."""
+    import torch
+
+    bins, offs = inputs_mod.random_csr(npix=500, T=4096, max_n=2500, seed=11)
+    zo = oracle_mod.sketch(bins, offs, 4096, 10)
+    db, do = _dev(bins), _dev(offs)
+    for mean_hint in (50, 300, 600, 2000, 0):
+        z = gpu.srt3d_sketch(db, do, 4096, 10, total_photons=mean_hint * 500 if mean_hint else None)
+        torch.cuda.synchronize()
+        _assert_sketch_close(_host(z), zo)
+
+
+def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):
+    """Segments starting at every residue mod 8, n = 0..17, non-zero offsets[0], odd bins base."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    T, m = 4613, 10
+    lists = [rng.integers(0, T, n) for n in list(range(18)) * 8]
+    bins, offs = _csr(lists)
+    zo = oracle_mod.sketch(bins, offs, T, m)
+    for shift in range(8):
+        pad = np.concatenate([rng.integers(0, T, shift).astype(np.uint16), bins])
+        db = _dev(pad)
+        # offsets relative to the padded array: offsets[0] = shift (sub-frame slice convention)
+        do = _dev((offs + shift).astype(np.uint32))
+        z = gpu.srt3d_sketch(db, do, T, m, total_photons=int(offs[-1]))
+        torch.cuda.synchronize()
+        _assert_sketch_close(_host(z), zo)
+        # base pointer misaligned by one photon (2 bytes): view of pad[1:]
+        db1 = db[1:]
+        do1 = _dev((offs + shift - 1).astype(np.uint32)) if shift >= 1 else None
+        if do1 is not None:
+            z = gpu.srt3d_sketch(db1, do1, T, m, total_photons=int(offs[-1]))
+            torch.cuda.synchronize()
+            _assert_sketch_close(_host(z), zo)
+
+
+def test_sketch_special_cases(gpu, oracle_mod):
+    """P1 single photon, P3 one photon per bin (blind), P4 closed forms, npix = 1, all empty."""
+    zg = _gpu_sketch(gpu, *_csr([[25]]), 100, 4)
+    np.testing.assert_allclose(zg[0], [1j, -1, -1j, 1], atol=1e-6)
+    for T in (16, 100, 1024, 8192):
+        zg = _gpu_sketch(gpu, *_csr([np.arange(T)]), T, min(T - 1, 64))
+        assert np.abs(zg).max() < 1e-5
+    zg = _gpu_sketch(gpu, *_csr([[0, 50], [0, 25, 50]]), 100, 6)
+    j = np.arange(1, 7)
+    np.testing.assert_allclose(zg[0], (1 + (-1.0) ** j) / 2, atol=1e-6)
+    np.testing.assert_allclose(zg[1][:2], [1j / 3, 1 / 3], atol=1e-6)
+    zg = _gpu_sketch(gpu, *_csr([[], [], []]), 100, 3, hint=False)
+    assert np.all(zg == 0)
+
+
+def test_sketch_empty_frame_and_errors(gpu):
+    """npix = 0 is a no-op; invalid arguments return error codes and write nothing."""
+    import torch
+
+    z = torch.full((4, 3), 7.0 + 7.0j, dtype=torch.complex64, device="cuda")
+    bins = _dev(np.array([1, 2, 3], dtype=np.uint16))
+    offs0 = _dev(np.zeros(1, dtype=np.uint32))
+    gpu.srt3d_sketch(bins, offs0, 100, 3, z=z[:0])
+    offs = _dev(np.array([0, 1, 2, 3, 3], dtype=np.uint32))
+    for T, m, code in [(1, 1, -1), (100, 0, -1), (100, 100, -1), (65537, 3, -1), (1000, 65, -3)]:
+        with pytest.raises(gpu.Srt3dError) as e:
+            gpu.srt3d_sketch(bins, offs, T, m, z=torch.empty((4, max(m, 1)), dtype=torch.complex64, device="cuda"))
+        assert e.value.code == code
+    lib = gpu.load_library()
+    import ctypes
+
+    rc = lib.srt3d_sketch(None, ctypes.c_void_p(offs.data_ptr()), 4, 100, 3, ctypes.c_void_p(z.data_ptr()), 3, None)
+    assert rc == -2
+    rc = lib.srt3d_sketch(ctypes.c_void_p(bins.data_ptr()), ctypes.c_void_p(offs.data_ptr() + 1), 4, 100, 3,
+                          ctypes.c_void_p(z.data_ptr()), 3, None)
+    assert rc == -5
+    torch.cuda.synchronize()
+    assert torch.all(z == 7.0 + 7.0j)
+
+
+def test_sketch_deterministic(gpu, inputs_mod):
+    import torch
+
+    bins, offs = inputs_mod.random_csr(npix=3000, T=8192, max_n=2000, seed=5)
+    db, do = _dev(bins), _dev(offs)
+    z1 = gpu.srt3d_sketch(db, do, 8192, 32, total_photons=int(offs[-1]))
+    z2 = gpu.srt3d_sketch(db, do, 8192, 32, total_photons=int(offs[-1]))
+    torch.cuda.synchronize()
+    assert torch.equal(z1, z2)
+
+
+def test_check_csr(gpu):
+    bins, offs = _csr([[1, 2], [3]])
+    assert gpu.srt3d_check_csr(_dev(bins), _dev(offs), 4) == 0
+    assert gpu.srt3d_check_csr(_dev(bins), _dev(offs), 3) != 0
+    assert gpu.srt3d_check_csr(_dev(bins), _dev(np.array([0, 2, 1], dtype=np.uint32)), 4) != 0
+
+
+# ------------------------------------------------------ expected sketch K2
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("T,m,sigma", [(1024, 4, 2.0), (4613, 10, 5.0), (2500, 20, 3.0), (8192, 32, 6.0),
+                                       (8192, 64, 0.0), (153, 10, 2.0), (65536, 37, 1.0), (7, 5, 0.5)])
+def test_expected_sketch_parity(gpu, oracle_mod, inputs_mod, K, T, m, sigma):
+    t, a = inputs_mod.random_theta(1000, K, T, seed=K * 31 + m)
+    t[:10] += np.float32(T) * np.arange(-5, 5, dtype=np.float32)[:, None]  # periodic in t (A16)
+    t[10:12] = np.float32(T) - np.float32(1e-3)
+    zg = _host(gpu.srt3d_expected_sketch(_dev(t), _dev(a), sigma, T, m))
+    zo = oracle_mod.expected_sketch(t, a, sigma, T, m)
+    _assert_sketch_close(zg, zo)
+
+
+# ----------------------------------------------------------- gradient K3
+def _grad_tol_check(z, t, a, sigma, T, m, gg, go):
+    """A12 per-component tolerance with the S-scaled floor, plus frame-level relative norms."""
+    gt_g, ga_g, L_g = gg
+    gt_o, ga_o, L_o = go
+    w = 2 * np.pi * np.arange(1, m + 1) / T
+    h = np.exp(-sigma**2 * w**2 / 2)
+    a64 = a.astype(np.float64)
+    mag = np.abs(z.astype(np.complex128)) + np.abs(a64).sum(1)[:, None] * h[None, :]  # |z_j| + sum_k |a_k| h_j
+    S_L = (mag**2).sum(1)
+    S_a = 2 * (h[None, :] * mag).sum(1)
+    S_t = 2 * np.abs(a64) * ((w * h)[None, :] * mag).sum(1)[:, None]
+    assert np.all(np.abs(L_g - L_o) <= 1e-4 * np.abs(L_o) + 1e-5 * S_L)
+    assert np.all(np.abs(ga_g - ga_o) <= 1e-4 * np.abs(ga_o) + 1e-5 * S_a[:, None])
+    assert np.all(np.abs(gt_g - gt_o) <= 1e-4 * np.abs(gt_o) + 1e-5 * S_t)
+    # frame level: ||delta||_2 <= 1e-4 ||ref||_2 + 1e-5 ||S||_2 (the floor matters only at the truth,
+    # where ref is itself fp32-rounding noise of z)
+    for g, o, S in ((gt_g, gt_o, S_t), (ga_g, ga_o, np.broadcast_to(S_a[:, None], ga_o.shape))):
+        assert np.linalg.norm(g - o) <= 1e-4 * np.linalg.norm(o) + 1e-5 * np.linalg.norm(S)
+    assert abs(L_g.sum() - L_o.sum()) <= 1e-4 * L_o.sum() + 1e-5 * S_L.sum()
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("T,m,sigma", [(1024, 4, 2.0), (4613, 10, 5.0), (2500, 20, 3.0), (8192, 32, 6.0),
+                                       (8192, 64, 6.0), (4613, 5, 5.0), (1000, 7, 0.0)])
+def test_sketch_grad_parity_random(gpu, oracle_mod, inputs_mod, K, T, m, sigma):
+    import torch
+
+    npix = 1337
+    t, a = inputs_mod.random_theta(npix, K, T, seed=K + 100 * m, alpha_lo=0.0, alpha_hi=1.0)
+    a[::7, -1] = 0.0  # absent surfaces
+    z = inputs_mod.random_sketch(npix, m, seed=K * m)
+    gt, ga, L = gpu.srt3d_sketch_grad(_dev(z), _dev(t), _dev(a), sigma, T, m)
+    torch.cuda.synchronize()
+    go = oracle_mod.sketch_grad(z, t, a, sigma, T, m)
+    _grad_tol_check(z, t, a, sigma, T, m, (_host(gt), _host(ga), _host(L)), go)
+    assert np.all(_host(gt)[::7, -1] == 0.0)  # G6: alpha_k = 0 -> g_t,k = 0 exactly
+
+
+@pytest.mark.parametrize("T,m,sigma,K", [(1024, 4, 2.0, 1), (8192, 32, 6.0, 3), (2500, 20, 3.0, 2)])
+def test_sketch_grad_near_truth(gpu, oracle_mod, inputs_mod, T, m, sigma, K):
+    """At and near the truth of a noiseless sketch the gradient is ~0: the S-scaled floor applies."""
+    import torch
+
+    t, a = inputs_mod.random_theta(2000, K, T, seed=77, alpha_lo=0.05, alpha_hi=1.0)
+    zt = gpu.srt3d_expected_sketch(_dev(t), _dev(a), sigma, T, m)
+    for dt in (0.0, 0.01, 10.0):
+        tt = (t + np.float32(dt)).astype(np.float32)
+        gt, ga, L = gpu.srt3d_sketch_grad(zt, _dev(tt), _dev(a), sigma, T, m)
+        torch.cuda.synchronize()
+        z = _host(zt)
+        go = oracle_mod.sketch_grad(z, tt, a, sigma, T, m)
+        _grad_tol_check(z, tt, a, sigma, T, m, (_host(gt), _host(ga), _host(L)), go)
+
+
+def test_grad_errors_write_nothing(gpu):
+    import torch
+
+    z = torch.zeros((4, 3), dtype=torch.complex64, device="cuda")
+    t = torch.zeros((4, 9), device="cuda")
+    gt = torch.full((4, 9), 5.0, device="cuda")
+    with pytest.raises(gpu.Srt3dError) as e:
+        gpu.srt3d_sketch_grad(z, t, t.clone(), 1.0, 100, 3, grad_t=gt, grad_alpha=gt.clone())
+    assert e.value.code == -3  # K = 9 > SRT3D_MAX_K
+    t = torch.zeros((4, 2), device="cuda")
+    for sigma, code in [(float("nan"), -1), (-1.0, -1)]:
+        with pytest.raises(gpu.Srt3dError) as e:
+            gpu.srt3d_sketch_grad(z, t, t.clone(), sigma, 100, 3)
+        assert e.value.code == code
+    with pytest.raises(gpu.Srt3dError) as e:
+        gpu.srt3d_descent_update(t, t.clone(), t.clone(), t.clone(), 1.0, 100, 3, eta=0.0)
+    assert e.value.code == -1
+    torch.cuda.synchronize()
+    assert torch.all(gt == 5.0)
+
+
+# ---------------------------------------------------------- update K4 / fused
+def test_update_parity_and_fused_step(gpu, oracle_mod, inputs_mod):
+    import torch
+
+    T, m, sigma, K = 8192, 32, 6.0, 3
+    t, a = inputs_mod.random_theta(3000, K, T, seed=4, alpha_lo=0.0, alpha_hi=1.0)
+    z = inputs_mod.random_sketch(3000, m, seed=4, scale=0.01)
+    dz, dt, da = _dev(z), _dev(t), _dev(a)
+    gt, ga, _ = gpu.srt3d_sketch_grad(dz, dt, da, sigma, T, m)
+    t1, a1 = dt.clone(), da.clone()
+    gpu.srt3d_descent_update(t1, a1, gt, ga, sigma, T, m, eta=0.5)
+    t2, a2 = dt.clone(), da.clone()
+    gpu.srt3d_sketch_grad_step(dz, t2, a2, sigma, T, m, eta=0.5)
+    torch.cuda.synchronize()
+    # fused kernel == grad + update, bitwise (same arithmetic, same order)
+    assert torch.equal(t1, t2) and torch.equal(a1, a2)
+    to, ao = oracle_mod.descent_update(t, a, _host(gt), _host(ga), sigma, T, m, eta=0.5)
+    tg = _host(t1).astype(np.float64)
+    dtw = np.abs(tg - to)
+    dtw = np.minimum(dtw, T - dtw)  # wrap-around
+    assert dtw.max() <= 2e-3  # fp32 ulp of t near T is 4.9e-4
+    assert np.abs(_host(a1) - ao).max() <= 1e-6
+
+
+def test_iterations_reduce_loss_c1(gpu, oracle_mod, inputs_mod):
+    """C1 end to end: sketch, then 20 iterations from t* + 10; loss falls and depths approach t*."""
+    import torch
+
+    f = inputs_mod.make_frame("C1")
+    t0, a0 = f.theta0()
+    z, t, a = gpu.fit_frame(_dev(f.bins), _dev(f.offsets), _dev(t0), _dev(a0), f.sigma, f.T, f.m, iters=f.iters,
+                            total_photons=f.n_photons)
+    torch.cuda.synchronize()
+    _assert_sketch_close(_host(z), oracle_mod.sketch(f.bins, f.offsets, f.T, f.m))
+    L0 = oracle_mod.sketch_grad(_host(z), t0, a0, f.sigma, f.T, f.m)[2].sum()
+    L1 = oracle_mod.sketch_grad(_host(z), _host(t), _host(a), f.sigma, f.T, f.m)[2].sum()
+    assert L1 < 0.5 * L0
+    err0 = np.abs(t0 - f.t_true).mean()
+    err1 = np.abs(_host(t) - f.t_true).mean()
+    assert err1 < 0.5 * err0
+
+
+# ------------------------------------------------ BASELINE configs (C1..C5, C4 sweep)
+def _sample_idx(npix, k, seed):
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([[0, npix - 1], rng.choice(npix, size=min(k, npix), replace=False)]))
+    return idx
+
+
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", None), ("C3", None), ("C5", None),
+                                    ("C4", 100), ("C4", 1000), ("C4", 10000), ("C4", 100000)])
+def test_config_parity_full_size(gpu, oracle_mod, inputs_mod, name, n):
+    """Full-size BASELINE configs, in the launch configuration bench.py uses (hinted regime):
+    sketch checked on sampled pixels against the oracle; gradient at theta0 on sampled pixels."""
+    import torch
+
+    f = inputs_mod.make_frame(name, n_per_pixel=n)
+    db, do = _dev(f.bins), _dev(f.offsets)
+    z = gpu.srt3d_sketch(db, do, f.T, f.m, total_photons=f.n_photons)
+    torch.cuda.synchronize()
+    zg = _host(z)
+    idx = _sample_idx(f.npix, 256 if f.n_photons / f.npix < 5000 else 24, seed=1)
+    sb, so = _sub_csr(f.bins, f.offsets, idx)
+    _assert_sketch_close(zg[idx], oracle_mod.sketch(sb, so, f.T, f.m))
+    if name != "C4":
+        t0, a0 = f.theta0()
+        gt, ga, L = gpu.srt3d_sketch_grad(z, _dev(t0), _dev(a0), f.sigma, f.T, f.m)
+        torch.cuda.synchronize()
+        go = oracle_mod.sketch_grad(zg[idx], t0[idx], a0[idx], f.sigma, f.T, f.m)
+        _grad_tol_check(zg[idx], t0[idx], a0[idx], f.sigma, f.T, f.m,
+                        (_host(gt)[idx], _host(ga)[idx], _host(L)[idx]), go)
