@@ -293,6 +293,30 @@ def run_srt3d(args):
                "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
                "ms_per_step": float(e2e_ms.item()) / args.e2e_steps}
 
+    # L2-cold per-launch time of the gradient kernel (outside the timed region):
+    # flush L2 (write 2x its size) before each launch, CUDA events around it.
+    grad_cold_ms = None
+    if f.iters > 0:
+        l2 = torch.cuda.get_device_properties(local).L2_cache_size
+        flush = torch.empty(2 * max(l2, 1 << 20) // 4, dtype=torch.float32, device="cuda")
+        tt, aa = pipe.t0.clone(), pipe.a0.clone()
+        times = []
+        with torch.cuda.stream(s):
+            for r in range(6):
+                flush.fill_(float(r))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                if pipe.fused:
+                    srt3d.srt3d_sketch_grad_step(pipe.z, tt, aa, f.sigma, f.T, f.m, 0.5)
+                else:
+                    srt3d.srt3d_sketch_grad(pipe.z, tt, aa, f.sigma, f.T, f.m, grad_t=pipe.gt, grad_alpha=pipe.ga,
+                                            want_loss=False)
+                e1.record(s)
+                times.append((e0, e1))
+        s.synchronize()
+        grad_cold_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in times[1:])
+        del flush
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -323,7 +347,10 @@ def run_srt3d(args):
                 "gbs": g_bytes / (per_iter * 1e-3) / 1e9, "frac_hbm": g_bytes / (per_iter * 1e-3) / 1e9 / hbm,
                 "tflops": g_flops / (per_iter * 1e-3) / 1e12,
                 "frac_fp32": g_flops / (per_iter * 1e-3) / fp32_peak,
-                "note": "per-iteration time includes graph-node launch gaps; z stays L2-resident across iterations"}
+                "note": "per-iteration time includes graph-node launch gaps; z stays L2-resident across iterations",
+                "cold_l2_ms_per_launch": grad_cold_ms,
+                "cold_l2_gbs": g_bytes / (grad_cold_ms * 1e-3) / 1e9 if grad_cold_ms else None,
+                "cold_l2_frac_hbm": g_bytes / (grad_cold_ms * 1e-3) / 1e9 / hbm if grad_cold_ms else None}
     # dominant kernel -> roofline object
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")

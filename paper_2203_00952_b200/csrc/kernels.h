@@ -6,7 +6,10 @@
 namespace srt3d {
 
 constexpr int SK_THREADS = 256;                 // sketch CTA size
-constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T <= 24576 uses the smem table)
+constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T < 24576 uses the smem table)
+#ifndef SK_TABLE_PERIOD
+#define SK_TABLE_PERIOD 0                        // every TP-th sketch term read from the table (0 = off)
+#endif
 constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 constexpr int MAX_M = 64;
 constexpr int MAX_K = 8;

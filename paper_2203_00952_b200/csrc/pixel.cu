@@ -12,6 +12,15 @@
 // range reduction), re-anchored every 32 frequencies from j*q_k; worst-case
 // phasor error 1.6e-6 (tools/sim_grad_phasor_error.py).
 // Per (j, k): 2 (phasor) + 1 (Phi) + 2 (gradient) packed FP32x2 instructions.
+//
+// Memory: each warp owns 32 consecutive pixels, whose z rows are one
+// contiguous slab of 32*m complex64.  The warp stages the slab into shared
+// memory with coalesced asynchronous copies (cp.async / LDGSTS, 16-byte units
+// for even m; all of a lane's copies in flight at once) into rows of padded
+// stride S, so that the per-thread row reads are bank-conflict free; the
+// expected-sketch output goes the same way in reverse.  (Reading z row-wise
+// straight from global memory touches 32 sectors per warp load — L1-wavefront
+// bound; a register-staged copy serialises load -> store.)
 #include <cstdint>
 
 #include "common.cuh"
@@ -19,17 +28,67 @@
 
 namespace srt3d {
 
-template <int M>
-struct ConstView {
-  const float* hh;
-  const float* wh;
-};
+// Row stride of the shared z tile, in complex64 units.  16-byte path (even
+// m): S = m + 2 keeps rows 16-byte aligned and makes the per-thread LDS.128
+// row reads conflict-free (16B-unit address 17*row + j/2 walks all 8 units of
+// a 128-byte phase for 8 consecutive rows).  8-byte path (odd m): S odd.
+__host__ __device__ constexpr int zstride(int m) { return (m & 1) ? m : m + 2; }
+
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, int bytes16) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  if (bytes16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Stage a warp's slab of nrows*m complex64 (contiguous in global memory) into
+// the padded shared tile with asynchronous copies (LDGSTS: every lane keeps
+// all its copies in flight; no register staging).  Units are 16 bytes (two
+// complex) when m is even, else 8 bytes.  Row/column advance incrementally.
+__device__ __forceinline__ void warp_slab_load(float2* tile, const float2* gsrc, int nrows, int m, int S, int lane) {
+  const bool v16 = (m & 1) == 0;
+  const int mu = v16 ? m / 2 : m;  // units per row
+  const int total = nrows * mu;
+  int row = lane / mu, col = lane - (lane / mu) * mu;
+  const int q = 32 / mu, r = 32 - (32 / mu) * mu;
+  const int w = v16 ? 2 : 1;
+  for (int u = lane; u < total; u += 32) {
+    cp_async(tile + row * S + col * w, gsrc + (size_t)u * w, v16);
+    col += r;
+    row += q;
+    if (col >= mu) {
+      col -= mu;
+      row++;
+    }
+  }
+  cp_async_wait_all();
+}
+
+// Coalesced copy-out of the warp's tile (expected sketch).
+__device__ __forceinline__ void warp_slab_store(const float2* tile, float2* gdst, int nrows, int m, int S, int lane) {
+  const int total = nrows * m;
+  int row = lane / m, col = lane - (lane / m) * m;
+  const int q = 32 / m, r = 32 - (32 / m) * m;
+#pragma unroll 4
+  for (int u = lane; u < total; u += 32) {
+    gdst[u] = tile[row * S + col];
+    col += r;
+    row += q;
+    if (col >= m) {
+      col -= m;
+      row++;
+    }
+  }
+}
 
 template <int K, int M, int MODE>
 __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
   // Frequency constants: compile-time-indexed kernel parameters when M is a
   // template constant; staged in shared memory for the runtime-m variant.
   __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
+  extern __shared__ float2 ztile[];
   if (M == 0 && MODE != PX_UPDATE) {
     for (int j = threadIdx.x; j < MAX_M; j += blockDim.x) {
       s_hh[j] = a.c.hh[j];
@@ -37,15 +96,29 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
     }
     __syncthreads();
   }
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.npix) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
+  if (row0 >= a.npix) return;
+  const long long i = row0 + lane;
+  const int nrows = (int)min(32ll, a.npix - row0);
   const int m = M ? M : (int)a.m;
+  const int S = zstride(m);
+  float2* tile = ztile + (size_t)warp * 32 * S;
+  if (MODE == PX_GRAD || MODE == PX_GRAD_STEP) {
+    warp_slab_load(tile, reinterpret_cast<const float2*>(a.z) + (size_t)row0 * m, nrows, m, S, lane);
+    __syncwarp();
+  }
+  // Lanes past the end of the frame compute a duplicate of the last pixel (so
+  // the warp stays converged for the slab copy-out) and store nothing.
+  const bool active = i < a.npix;
+  if (MODE != PX_EXPECTED && !active) return;
+  const long long ie = active ? i : a.npix - 1;
 
   float tk[K], ak[K];
 #pragma unroll
   for (int k = 0; k < K; k++) {
-    tk[k] = a.t_in[i * K + k];
-    ak[k] = a.a_in[i * K + k];
+    tk[k] = a.t_in[ie * K + k];
+    ak[k] = a.a_in[ie * K + k];
   }
 
   if (MODE == PX_UPDATE) {
@@ -83,8 +156,7 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
     GA[k] = 0ull;
     GT[k] = 0ull;
   }
-  const float2* zrow = reinterpret_cast<const float2*>(a.z) + (size_t)i * m;
-  float2* zout = reinterpret_cast<float2*>(a.zout) + (size_t)i * m;
+  float2* zrow = tile + lane * S;
 
 #pragma unroll(M ? M : 1)
   for (int j = 0; j < m; j++) {  // frequency j+1
@@ -102,17 +174,23 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
     }
     const float hh = M ? a.c.hh[j] : s_hh[j];
     // S = sum_k alpha_k p_jk  (Phi_j = hh * S)
-    u64 S = fmul2(pk(ak[0], ak[0]), P[0]);
+    u64 Sk = fmul2(pk(ak[0], ak[0]), P[0]);
 #pragma unroll
-    for (int k = 1; k < K; k++) S = ffma2(pk(ak[k], ak[k]), P[k], S);
+    for (int k = 1; k < K; k++) Sk = ffma2(pk(ak[k], ak[k]), P[k], Sk);
     if (MODE == PX_EXPECTED) {
-      zout[j] = make_float2(hh * lo_of(S), hh * hi_of(S));
+      zrow[j] = make_float2(hh * lo_of(Sk), hh * hi_of(Sk));
       continue;
     }
     const float wh = M ? a.c.wh[j] : s_wh[j];
-    const float2 zj = __ldg(zrow + j);
-    const float rr = fmaf(-hh, lo_of(S), zj.x);
-    const float ri = fmaf(-hh, hi_of(S), zj.y);
+    float2 zj;
+    if (M > 0 && (M & 1) == 0) {  // LDS.128: z_j, z_{j+1} (conflict-free with S = m + 2)
+      const float4 z2 = *reinterpret_cast<const float4*>(zrow + (j & ~1));
+      zj = (j & 1) ? make_float2(z2.z, z2.w) : make_float2(z2.x, z2.y);
+    } else {
+      zj = zrow[j];
+    }
+    const float rr = fmaf(-hh, lo_of(Sk), zj.x);
+    const float ri = fmaf(-hh, hi_of(Sk), zj.y);
     L = fmaf(rr, rr, fmaf(ri, ri, L));
     const u64 RHO = pk(hh * rr, hh * ri);   // hhat_j r_j
     const u64 SIG = pk(wh * rr, -wh * ri);  // omega_j hhat_j (r_r, -r_i)
@@ -122,7 +200,11 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
       GT[k] = ffma2(SIG, pk(hi_of(P[k]), lo_of(P[k])), GT[k]);     // (s_r p_i, -s_i p_r)
     }
   }
-  if (MODE == PX_EXPECTED) return;
+  if (MODE == PX_EXPECTED) {  // coalesced copy-out of the warp's slab
+    __syncwarp();
+    warp_slab_store(tile, reinterpret_cast<float2*>(a.zout) + (size_t)row0 * m, nrows, m, S, lane);
+    return;
+  }
 
   float gt[K], ga[K];
 #pragma unroll
@@ -157,7 +239,15 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
 template <int K, int M, int MODE>
 static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
   const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
-  pixel_kernel<K, M, MODE><<<(unsigned)grid, PX_THREADS, 0, s>>>(a);
+  const size_t smem = MODE == PX_UPDATE ? 0 : sizeof(float2) * (PX_THREADS / 32) * 32 * zstride(M ? M : (int)a.m);
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set && MODE != PX_UPDATE) {
+    cudaError_t e = cudaFuncSetAttribute(pixel_kernel<K, M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(float2) * (PX_THREADS / 32) * 32 * zstride(MAX_M)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  pixel_kernel<K, M, MODE><<<(unsigned)grid, PX_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -38,7 +38,7 @@ __global__ void check_csr_kernel(const uint16_t* __restrict__ bins, const uint32
 }
 
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms) {
-  const bool tab = (size_t)a.T * sizeof(float2) <= SK_MAX_SMEM;
+  const bool tab = ((size_t)a.T + 1) * sizeof(float2) <= SK_MAX_SMEM;
   if (!tab) return launch_sketch_g32(M, false, a, s, num_sms);
   switch (G) {
     case 4:

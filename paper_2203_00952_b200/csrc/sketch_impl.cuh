@@ -30,10 +30,14 @@
 namespace srt3d {
 
 // exp(i 2 pi r / T) for r < T into shared memory, fp64 sincospi on the
-// centred index so the argument stays in (-1, 1].
+// centred index so the argument stays in (-1, 1]; tab[T] = 0 (absent photon).
 __device__ __forceinline__ void build_phase_table(float2* tab, uint32_t T) {
   const double s = 2.0 / (double)T;
-  for (uint32_t r = threadIdx.x; r < T; r += blockDim.x) {
+  for (uint32_t r = threadIdx.x; r <= T; r += blockDim.x) {
+    if (r == T) {
+      tab[r] = make_float2(0.f, 0.f);
+      continue;
+    }
     int rc = (2u * r > T) ? (int)r - (int)T : (int)r;
     double sn, cs;
     sincospi(s * (double)rc, &sn, &cs);
@@ -49,7 +53,23 @@ __device__ __forceinline__ float2 phasor_exact(uint32_t r, uint32_t T) {
   return make_float2((float)cs, (float)sn);
 }
 
-template <int M, bool TAB>
+// (n mod T) for n < 2^23 without an integer division: fp32 quotient estimate
+// (n exact in fp32) corrected by at most one step either way.
+__device__ __forceinline__ uint32_t mod_small(uint32_t n, uint32_t T, float invT) {
+  uint32_t q = __float2uint_rz(__uint2float_rz(n) * invT);
+  int r = (int)n - (int)(q * T);
+  if (r < 0) r += (int)T;
+  if (r >= (int)T) r -= (int)T;
+  return (uint32_t)r;
+}
+
+// Per-lane accumulators of one pass (M frequencies) over a pixel's photons.
+// TP = table period: with TP > 0 every TP-th term is read from the exact
+// phase table (index advanced by d = TP*x mod T on the ALU pipe) instead of
+// one more complex multiply; this moves work off the FP32 pipe (FADD2 only)
+// and re-anchors the chain.  The table carries a zero entry at index T,
+// used as the "absent photon" (keeps one copy of the unrolled body).
+template <int M, bool TAB, int TP>
 struct PhotonAcc {
   u64 acc[M];
   __device__ __forceinline__ void zero() {
@@ -60,39 +80,78 @@ struct PhotonAcc {
     if (TAB) return tab[r];
     return phasor_exact(r, T);
   }
-  // one photon
-  __device__ __forceinline__ void add1(const float2* tab, uint32_t x, uint32_t T, uint32_t j0) {
-    float2 w = base(tab, x, T);
-    u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
-    u64 P = W;
-    if (j0) {
-      float2 a = base(tab, phase_index(x, j0 + 1, T), T);
-      P = pk(a.x, a.y);
-    }
-    acc[0] = fadd2(acc[0], P);
-#pragma unroll
-    for (int j = 1; j < M; j++) {
-      P = cmul2(P, W, Wn);
-      acc[j] = fadd2(acc[j], P);
-    }
+  __device__ __forceinline__ static u64 lds64(const float2* tab, uint32_t boff) {
+    const float2 v = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(tab) + boff);
+    return pk(v.x, v.y);
   }
-  // two photons, interleaved chains (ILP 2)
-  __device__ __forceinline__ void add2(const float2* tab, uint32_t x, uint32_t y, uint32_t T, uint32_t j0) {
-    float2 w = base(tab, x, T), v = base(tab, y, T);
-    u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
-    u64 V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
+  // Two photons x, y as interleaved chains (ILP 2).  If !yvalid the second
+  // chain uses the zero table entry / w = 0 and contributes exactly 0.
+  __device__ __forceinline__ void add2(const float2* tab, uint32_t x, uint32_t y, bool yvalid, uint32_t T,
+                                       uint32_t j0, float invT) {
+    if (!TAB) {
+      float2 w = phasor_exact(x, T), v = phasor_exact(y, T);
+      if (!yvalid) v = make_float2(0.f, 0.f);
+      const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x), V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
+      u64 P = W, Q = V;
+      if (j0) {
+        const float2 pa = phasor_exact(phase_index(x, j0 + 1, T), T);
+        float2 qa = phasor_exact(phase_index(y, j0 + 1, T), T);
+        if (!yvalid) qa = make_float2(0.f, 0.f);
+        P = pk(pa.x, pa.y);
+        Q = pk(qa.x, qa.y);
+      }
+      acc[0] = fadd2(acc[0], fadd2(P, Q));
+#pragma unroll
+      for (int j = 1; j < M; j++) {
+        P = cmul2(P, W, Wn);
+        Q = cmul2(Q, V, Vn);
+        acc[j] = fadd2(acc[j], fadd2(P, Q));
+      }
+      return;
+    }
+    const uint32_t yy = yvalid ? y : T;  // tab[T] = 0
+    const float2 w = tab[x], v = tab[yy];
+    const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x), V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
+    // byte offsets of the current anchor index r_j = (j x) mod T, and the TP step
+    uint32_t rx = x * 8u, ry = yy * 8u;
     u64 P = W, Q = V;
     if (j0) {
-      float2 a = base(tab, phase_index(x, j0 + 1, T), T);
-      float2 b = base(tab, phase_index(y, j0 + 1, T), T);
-      P = pk(a.x, a.y);
-      Q = pk(b.x, b.y);
+      rx = mod_small((j0 + 1) * x, T, invT) * 8u;
+      ry = yvalid ? mod_small((j0 + 1) * y, T, invT) * 8u : T * 8u;
+      P = lds64(tab, rx);
+      Q = lds64(tab, ry);
+    }
+    uint32_t dx = 0, dy = 0, dxT = 0, dyT = 0;
+    if (TP > 0) {
+      dx = mod_small(TP * x, T, invT) * 8u;
+      dy = yvalid ? mod_small(TP * y, T, invT) * 8u : 0u;
+      dxT = dx - 8u * T;                  // r + d - T (mod 2^32)
+      dyT = yvalid ? dy - 8u * T : 0u;
+    }
+    // the next anchor is fetched one period ahead (hides the LDS latency)
+    u64 Pn = 0ull, Qn = 0ull;
+    if (TP > 0 && TP < M) {
+      rx = min(rx + dx, rx + dxT);  // unsigned: (r + d) mod T, scaled by 8
+      ry = min(ry + dy, ry + dyT);
+      Pn = lds64(tab, rx);
+      Qn = lds64(tab, ry);
     }
     acc[0] = fadd2(acc[0], fadd2(P, Q));
 #pragma unroll
     for (int j = 1; j < M; j++) {
-      P = cmul2(P, W, Wn);
-      Q = cmul2(Q, V, Vn);
+      if (TP > 0 && (j % TP) == 0) {
+        P = Pn;
+        Q = Qn;
+        if (j + TP < M) {
+          rx = min(rx + dx, rx + dxT);
+          ry = min(ry + dy, ry + dyT);
+          Pn = lds64(tab, rx);
+          Qn = lds64(tab, ry);
+        }
+      } else {
+        P = cmul2(P, W, Wn);
+        Q = cmul2(Q, V, Vn);
+      }
       acc[j] = fadd2(acc[j], fadd2(P, Q));
     }
   }
@@ -115,7 +174,7 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int gl) {
   }
 }
 
-template <int M, int G, bool TAB>
+template <int M, int G, bool TAB, int TP>
 __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
   extern __shared__ float2 tab[];
   if (TAB) {
@@ -138,6 +197,7 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(a.bins - off0);
   const uint16_t* __restrict__ bins = a.bins;
   const uint32_t T = a.T, j0 = a.j0;
+  const float invT = 1.0f / (float)a.T;
 
   for (long long tile = warp0; tile < ntiles; tile += nwarps) {
     const long long pix = tile * PPW + grp;
@@ -159,11 +219,20 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
       cb = (long long)(asb >> 3);
       ce = (long long)(ase >> 3);
     }
-    PhotonAcc<M, TAB> pa;
+    PhotonAcc<M, TAB, TP> pa;
     pa.zero();
-    // scalar head and tail peel (< 8 photons each)
-    for (unsigned long long p = beg + gl; p < hend; p += G) pa.add1(tab, bins[p], T, j0);
-    for (unsigned long long p = tbeg + gl; p < end; p += G) pa.add1(tab, bins[p], T, j0);
+    // scalar head + tail peel (< 8 photons each), processed in pairs through
+    // the same add2 body as the vector loop
+    {
+      const int nh = (int)(hend - beg), nt = (int)(end - tbeg), nht = nh + nt;
+      for (int idx = gl; idx < nht; idx += 2 * G) {
+        const int idy = idx + G;
+        const unsigned long long px = idx < nh ? beg + idx : tbeg + (idx - nh);
+        const bool yv = idy < nht;
+        const unsigned long long py = yv ? (idy < nh ? beg + idy : tbeg + (idy - nh)) : px;
+        pa.add2(tab, bins[px], bins[py], yv, T, j0, invT);
+      }
+    }
 
     // warp-uniform number of super-chunks
     const long long nchunks = ce - cb;
@@ -177,16 +246,18 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
     for (int i = 0; i < VL; i++) res[i] = 0.f;
 
     for (int sc = 0; sc < nsc; sc++) {
-      const long long c0 = cb + (long long)sc * G * CPL;
-#pragma unroll 2
-      for (int k = 0; k < CPL; k++) {
-        const long long c = c0 + gl + (long long)k * G;
-        if (c < ce) {
-          uint4 v = __ldg(vb + c);
-          pa.add2(tab, v.x & 0xffffu, v.x >> 16, T, j0);
-          pa.add2(tab, v.y & 0xffffu, v.y >> 16, T, j0);
-          pa.add2(tab, v.z & 0xffffu, v.z >> 16, T, j0);
-          pa.add2(tab, v.w & 0xffffu, v.w >> 16, T, j0);
+      const long long cend = min(ce, cb + (long long)(sc + 1) * G * CPL);
+      long long c = cb + (long long)sc * G * CPL + gl;
+      uint4 nxt = make_uint4(0, 0, 0, 0);
+      if (c < cend) nxt = __ldg(vb + c);
+#pragma unroll 1
+      for (; c < cend; c += G) {
+        const uint4 v = nxt;
+        if (c + G < cend) nxt = __ldg(vb + c + G);  // prefetch the lane's next 16B chunk
+#pragma unroll 1
+        for (int h = 0; h < 4; h++) {
+          const uint32_t wv = h == 0 ? v.x : (h == 1 ? v.y : (h == 2 ? v.z : v.w));
+          pa.add2(tab, wv & 0xffffu, wv >> 16, true, T, j0, invT);
         }
       }
       float f[NVP];
@@ -216,10 +287,10 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
 }
 
 // ---- host-side dispatch ---------------------------------------------------
-template <int M, int G, bool TAB>
+template <int M, int G, bool TAB, int TP>
 static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
-  auto fn = sketch_kernel<M, G, TAB>;
-  const size_t smem = TAB ? sizeof(float2) * a.T : 0;
+  auto fn = sketch_kernel<M, G, TAB, TP>;
+  const size_t smem = TAB ? sizeof(float2) * (a.T + 1) : 0;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_MAX_SMEM);
@@ -240,12 +311,12 @@ static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_
   return cudaGetLastError();
 }
 
-template <int G, bool TAB>
+template <int G, bool TAB, int TP>
 static cudaError_t dispatch_m(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
   switch (M) {
 #define SRT3D_CASE(MM) \
   case MM:             \
-    return launch_sketch_t<MM, G, TAB>(a, s, num_sms);
+    return launch_sketch_t<MM, G, TAB, TP>(a, s, num_sms);
     SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
     SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
     SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)
