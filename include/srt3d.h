@@ -82,6 +82,26 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
                  float* z, uint64_t total_photons_hint, void* stream);
 
 /*
+ * srt3d_sketch_ex — srt3d_sketch with the launch regime chosen explicitly
+ * (same result up to fp32 rounding order; used by tests and tuning):
+ *   path            SRT3D_PATH_AUTO (0): bin-count when the mean photon count
+ *                   per pixel is >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * T and
+ *                   the histogram fits in shared memory, else direct;
+ *                   SRT3D_PATH_DIRECT (1): per-photon complex recurrence;
+ *                   SRT3D_PATH_BINCOUNT (2): per-pixel shared-memory
+ *                   histogram h[x] then z_j = (1/n) sum_x h[x] e^{i 2 pi j x/T}
+ *                   (the same sum as Eq. (3) regrouped by bin; T <= ~17000,
+ *                   else SRT3D_EUNSUPPORTED).
+ *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path only).
+ */
+#define SRT3D_PATH_AUTO 0
+#define SRT3D_PATH_DIRECT 1
+#define SRT3D_PATH_BINCOUNT 2
+#define SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN 1.0
+int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
+                    uint64_t total_photons_hint, int path, int lanes_per_pixel, void* stream);
+
+/*
  * srt3d_expected_sketch — Eq. (4) at omega_j = 2*pi*j/T with
  * the Gaussian IRF hhat(w) = exp(-sigma^2 w^2 / 2) (BASELINE.json north_star):
  *     z[i][j-1] = sum_{k<K} alpha[i][k] * hhat(omega_j) * exp(i omega_j t[i][k]).

@@ -32,7 +32,9 @@ _lib = None
 
 SRT3D_OK = 0
 ERRORS = {-1: "SRT3D_EINVAL", -2: "SRT3D_ENULL", -3: "SRT3D_EUNSUPPORTED", -4: "SRT3D_ECUDA", -5: "SRT3D_EALIGN"}
-EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_expected_sketch", "srt3d_sketch_grad",
+PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT = 0, 1, 2
+EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
+           "srt3d_sketch_grad",
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index")
 
 
@@ -58,6 +60,7 @@ def load_library(path: str | None = None):
     lib.srt3d_last_error.argtypes = []
     lib.srt3d_last_error.restype = ctypes.c_char_p
     lib.srt3d_sketch.argtypes = [P, P, i64, u32, u32, P, u64, P]
+    lib.srt3d_sketch_ex.argtypes = [P, P, i64, u32, u32, P, u64, ctypes.c_int, ctypes.c_int, P]
     lib.srt3d_expected_sketch.argtypes = [P, P, i64, u32, f32, u32, u32, P, P]
     lib.srt3d_sketch_grad.argtypes = [P, P, P, i64, u32, f32, u32, u32, P, P, P, P]
     lib.srt3d_descent_update.argtypes = [P, P, P, P, i64, u32, f32, u32, u32, f32, P]
@@ -104,6 +107,20 @@ def srt3d_sketch(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: t
     assert bins.dtype == torch.uint16 and offsets.dtype == torch.uint32 and z.dtype == torch.complex64
     hint = int(total_photons) if total_photons is not None else 0
     _call("srt3d_sketch", _ptr(bins), _ptr(offsets), npix, T, m, _ptr(z), hint, _stream(stream))
+    return z
+
+
+def srt3d_sketch_ex(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: torch.Tensor | None = None,
+                    total_photons: int | None = None, path: int = PATH_AUTO, lanes_per_pixel: int = 0,
+                    stream=None) -> torch.Tensor:
+    """Eq. (3) with the launch regime chosen explicitly (PATH_DIRECT / PATH_BINCOUNT, lanes 4..32)."""
+    npix = offsets.numel() - 1
+    if z is None:
+        z = torch.empty((max(npix, 0), m), dtype=torch.complex64, device=offsets.device)
+    _need_cuda(bins, offsets, z)
+    hint = int(total_photons) if total_photons is not None else 0
+    _call("srt3d_sketch_ex", _ptr(bins), _ptr(offsets), npix, T, m, _ptr(z), hint, int(path), int(lanes_per_pixel),
+          _stream(stream))
     return z
 
 

@@ -101,19 +101,27 @@ int srt3d_version(void) { return 100; }
 
 const char* srt3d_last_error(void) { return g_err; }
 
-int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
-                 uint64_t total_photons_hint, void* stream) {
+int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
+                    uint64_t total_photons_hint, int path, int lanes_per_pixel, void* stream) {
   if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
   int rc = check_tm(T, m);
   if (rc) return rc;
+  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_BINCOUNT) return fail(SRT3D_EINVAL, "path=%d unknown", path);
+  if (lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 && lanes_per_pixel != 16 &&
+      lanes_per_pixel != 32)
+    return fail(SRT3D_EINVAL, "lanes_per_pixel=%d must be 0, 4, 8, 16 or 32", lanes_per_pixel);
   if (npix == 0) return SRT3D_OK;
   if (!offsets || !z) return fail(SRT3D_ENULL, "offsets/z must be non-NULL");
   if (!bins && total_photons_hint != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
   if (!aligned(bins, 2) || !aligned(offsets, 4) || !aligned(z, 8))
     return fail(SRT3D_EALIGN, "bins/offsets/z must be 2/4/8-byte aligned");
+  const int M0 = (int)(m < 32 ? m : 32);
+  const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
+  if (path == SRT3D_PATH_BINCOUNT && !hist_fits)
+    return fail(SRT3D_EUNSUPPORTED, "bin-count path needs T <= ~17000 (T=%u)", T);
   cudaStream_t s = (cudaStream_t)stream;
   uint64_t total = total_photons_hint;
-  if (total == 0) {
+  if (total == 0 && (path == SRT3D_PATH_AUTO || lanes_per_pixel == 0)) {
     uint32_t ends[2] = {0, 0};
     cudaError_t e = cudaMemcpyAsync(&ends[0], offsets, 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&ends[1], offsets + npix, 4, cudaMemcpyDeviceToHost, s);
@@ -122,7 +130,11 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
     total = ends[1] >= ends[0] ? (uint64_t)(ends[1] - ends[0]) : 0;
   }
   if (!bins && total != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
-  const int G = lanes_for((double)total / (double)npix);
+  const double mean = (double)total / (double)npix;
+  if (path == SRT3D_PATH_AUTO)
+    path = (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) ? SRT3D_PATH_BINCOUNT
+                                                                                : SRT3D_PATH_DIRECT;
+  const int G = lanes_per_pixel ? lanes_per_pixel : lanes_for(mean);
   const int nsm = num_sms_current();
   srt3d::SketchArgs a;
   a.bins = bins ? bins : reinterpret_cast<const uint16_t*>(offsets);  // never dereferenced when no photons
@@ -134,10 +146,16 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
   for (uint32_t j0 = 0; j0 < m; j0 += 32) {
     a.j0 = j0;
     const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
-    cudaError_t e = srt3d::launch_sketch_pass(M, G, a, s, nsm);
+    cudaError_t e = path == SRT3D_PATH_BINCOUNT ? srt3d::launch_sketch_hist(M, a, s, nsm)
+                                                : srt3d::launch_sketch_pass(M, G, a, s, nsm);
     if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
   }
   return SRT3D_OK;
+}
+
+int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
+                 uint64_t total_photons_hint, void* stream) {
+  return srt3d_sketch_ex(bins, offsets, npix, T, m, z, total_photons_hint, SRT3D_PATH_AUTO, 0, stream);
 }
 
 int srt3d_expected_sketch(const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,

@@ -56,6 +56,8 @@ struct PixArgs {
 enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3 };
 
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms);
+cudaError_t launch_sketch_hist(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
+size_t sketch_hist_smem(uint32_t T, int M);
 cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, uint32_t m, uint32_t* r,
                                cudaStream_t s, int num_sms);
 cudaError_t launch_check_csr(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,

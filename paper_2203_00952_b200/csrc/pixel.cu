@@ -42,12 +42,14 @@ __device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, int b
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // Stage a warp's slab of nrows*m complex64 (contiguous in global memory) into
 // the padded shared tile with asynchronous copies (LDGSTS: every lane keeps
 // all its copies in flight; no register staging).  Units are 16 bytes (two
 // complex) when m is even, else 8 bytes.  Row/column advance incrementally.
-__device__ __forceinline__ void warp_slab_load(float2* tile, const float2* gsrc, int nrows, int m, int S, int lane) {
+__device__ __forceinline__ void warp_slab_issue(float2* tile, const float2* gsrc, int nrows, int m, int S, int lane) {
   const bool v16 = (m & 1) == 0;
   const int mu = v16 ? m / 2 : m;  // units per row
   const int total = nrows * mu;
@@ -63,7 +65,6 @@ __device__ __forceinline__ void warp_slab_load(float2* tile, const float2* gsrc,
       row++;
     }
   }
-  cp_async_wait_all();
 }
 
 // Coalesced copy-out of the warp's tile (expected sketch).
@@ -83,61 +84,34 @@ __device__ __forceinline__ void warp_slab_store(const float2* tile, float2* gdst
   }
 }
 
-template <int K, int M, int MODE>
-__global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
-  // Frequency constants: compile-time-indexed kernel parameters when M is a
-  // template constant; staged in shared memory for the runtime-m variant.
-  __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
-  extern __shared__ float2 ztile[];
-  if (M == 0 && MODE != PX_UPDATE) {
-    for (int j = threadIdx.x; j < MAX_M; j += blockDim.x) {
-      s_hh[j] = a.c.hh[j];
-      s_wh[j] = a.c.wh[j];
-    }
-    __syncthreads();
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
-  if (row0 >= a.npix) return;
-  const long long i = row0 + lane;
-  const int nrows = (int)min(32ll, a.npix - row0);
-  const int m = M ? M : (int)a.m;
-  const int S = zstride(m);
-  float2* tile = ztile + (size_t)warp * 32 * S;
-  if (MODE == PX_GRAD || MODE == PX_GRAD_STEP) {
-    warp_slab_load(tile, reinterpret_cast<const float2*>(a.z) + (size_t)row0 * m, nrows, m, S, lane);
-    __syncwarp();
-  }
-  // Lanes past the end of the frame compute a duplicate of the last pixel (so
-  // the warp stays converged for the slab copy-out) and store nothing.
-  const bool active = i < a.npix;
-  if (MODE != PX_EXPECTED && !active) return;
-  const long long ie = active ? i : a.npix - 1;
+// The harness update (reading A13) for one (pixel, k); shared by the fused
+// step and K4 so both produce bit-identical results.
+__device__ __forceinline__ void update_one(const PixArgs& a, float tk, float ak, float gt, float ga, float& tn,
+                                           float& an) {
+  const float am = fmaxf(ak, 0.05f);
+  float step = a.eta * gt * a.upd_t_scale / (am * am);
+  step = fminf(fmaxf(step, -a.max_step), a.max_step);
+  tn = tk - step;
+  tn = tn - a.Tf * floorf(tn / a.Tf);
+  if (tn >= a.Tf) tn -= a.Tf;
+  if (tn < 0.f) tn += a.Tf;
+  an = fminf(fmaxf(ak - a.eta * ga * a.upd_a_scale, 0.f), 1.f);
+}
 
+// One pixel: anchors, the j loop, and the mode's outputs.  zrow points at the
+// pixel's z row in the shared tile (row stride S).  `active` lanes store;
+// inactive lanes (past the end of the frame) compute a duplicate and store
+// nothing (PX_EXPECTED writes its tile row, copied out by the caller).
+template <int K, int M, int MODE>
+__device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool active, float2* zrow,
+                                           const float* s_hh, const float* s_wh) {
+  const int m = M ? M : (int)a.m;
   float tk[K], ak[K];
 #pragma unroll
   for (int k = 0; k < K; k++) {
-    tk[k] = a.t_in[ie * K + k];
-    ak[k] = a.a_in[ie * K + k];
+    tk[k] = a.t_in[i * K + k];
+    ak[k] = a.a_in[i * K + k];
   }
-
-  if (MODE == PX_UPDATE) {
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-      const float gt = a.grad_t[i * K + k], ga = a.grad_a[i * K + k];
-      const float am = fmaxf(ak[k], 0.05f);
-      float step = a.eta * gt * a.upd_t_scale / (am * am);
-      step = fminf(fmaxf(step, -a.max_step), a.max_step);
-      float tn = tk[k] - step;
-      tn = tn - a.Tf * floorf(tn / a.Tf);
-      if (tn >= a.Tf) tn -= a.Tf;
-      if (tn < 0.f) tn += a.Tf;
-      a.t_out[i * K + k] = tn;
-      a.a_out[i * K + k] = fminf(fmaxf(ak[k] - a.eta * ga * a.upd_a_scale, 0.f), 1.f);
-    }
-    return;
-  }
-
   uint32_t q[K];
   u64 W[K], Wn[K], P[K];
 #pragma unroll
@@ -156,7 +130,6 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
     GA[k] = 0ull;
     GT[k] = 0ull;
   }
-  float2* zrow = tile + lane * S;
 
 #pragma unroll(M ? M : 1)
   for (int j = 0; j < m; j++) {  // frequency j+1
@@ -173,7 +146,7 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
       }
     }
     const float hh = M ? a.c.hh[j] : s_hh[j];
-    // S = sum_k alpha_k p_jk  (Phi_j = hh * S)
+    // Sk = sum_k alpha_k p_jk  (Phi_j = hh * Sk)
     u64 Sk = fmul2(pk(ak[0], ak[0]), P[0]);
 #pragma unroll
     for (int k = 1; k < K; k++) Sk = ffma2(pk(ak[k], ak[k]), P[k], Sk);
@@ -196,15 +169,11 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
     const u64 SIG = pk(wh * rr, -wh * ri);  // omega_j hhat_j (r_r, -r_i)
 #pragma unroll
     for (int k = 0; k < K; k++) {
-      GA[k] = ffma2(RHO, P[k], GA[k]);                             // (rho_r p_r, rho_i p_i)
-      GT[k] = ffma2(SIG, pk(hi_of(P[k]), lo_of(P[k])), GT[k]);     // (s_r p_i, -s_i p_r)
+      GA[k] = ffma2(RHO, P[k], GA[k]);                          // (rho_r p_r, rho_i p_i)
+      GT[k] = ffma2(SIG, pk(hi_of(P[k]), lo_of(P[k])), GT[k]);  // (s_r p_i, -s_i p_r)
     }
   }
-  if (MODE == PX_EXPECTED) {  // coalesced copy-out of the warp's slab
-    __syncwarp();
-    warp_slab_store(tile, reinterpret_cast<float2*>(a.zout) + (size_t)row0 * m, nrows, m, S, lane);
-    return;
-  }
+  if (MODE == PX_EXPECTED || !active) return;
 
   float gt[K], ga[K];
 #pragma unroll
@@ -221,33 +190,128 @@ __global__ void __launch_bounds__(PX_THREADS) pixel_kernel(const PixArgs a) {
     }
     return;
   }
-  // PX_GRAD_STEP: fused update (same arithmetic as PX_UPDATE)
+  // PX_GRAD_STEP: fused update
 #pragma unroll
   for (int k = 0; k < K; k++) {
-    const float am = fmaxf(ak[k], 0.05f);
-    float step = a.eta * gt[k] * a.upd_t_scale / (am * am);
-    step = fminf(fmaxf(step, -a.max_step), a.max_step);
-    float tn = tk[k] - step;
-    tn = tn - a.Tf * floorf(tn / a.Tf);
-    if (tn >= a.Tf) tn -= a.Tf;
-    if (tn < 0.f) tn += a.Tf;
+    float tn, an;
+    update_one(a, tk[k], ak[k], gt[k], ga[k], tn, an);
     a.t_out[i * K + k] = tn;
-    a.a_out[i * K + k] = fminf(fmaxf(ak[k] - a.eta * ga[k] * a.upd_a_scale, 0.f), 1.f);
+    a.a_out[i * K + k] = an;
   }
+}
+
+template <int M>
+__device__ __forceinline__ void stage_consts(const PixArgs& a, float* s_hh, float* s_wh) {
+  if (M == 0) {
+    for (int j = threadIdx.x; j < MAX_M; j += blockDim.x) {
+      s_hh[j] = a.c.hh[j];
+      s_wh[j] = a.c.wh[j];
+    }
+    __syncthreads();
+  }
+}
+
+// Expected sketch (K2): one warp = 32 pixels, output staged through the
+// padded tile and copied out coalesced.
+template <int K, int M>
+__global__ void __launch_bounds__(PX_THREADS) expected_kernel(const PixArgs a) {
+  __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
+  extern __shared__ float2 ztile[];
+  stage_consts<M>(a, s_hh, s_wh);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
+  if (row0 >= a.npix) return;
+  const long long i = row0 + lane;
+  const int nrows = (int)min(32ll, a.npix - row0);
+  const int m = M ? M : (int)a.m;
+  const int S = zstride(m);
+  float2* tile = ztile + (size_t)warp * 32 * S;
+  const bool active = i < a.npix;
+  pixel_body<K, M, PX_EXPECTED>(a, active ? i : a.npix - 1, active, tile + lane * S, s_hh, s_wh);
+  __syncwarp();
+  warp_slab_store(tile, reinterpret_cast<float2*>(a.zout) + (size_t)row0 * m, nrows, m, S, lane);
+}
+
+// Gradient / fused step (K3, K3+K4): one warp = 32 pixels; the warp's z slab
+// is staged into its shared tile with cp.async, then each lane runs its pixel.
+template <int K, int M, int MODE>
+__global__ void __launch_bounds__(PX_THREADS) grad_kernel(const PixArgs a) {
+  __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
+  extern __shared__ float2 ztile[];
+  stage_consts<M>(a, s_hh, s_wh);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
+  if (row0 >= a.npix) return;
+  const int m = M ? M : (int)a.m;
+  const int S = zstride(m);
+  float2* tile = ztile + (size_t)warp * 32 * S;
+  warp_slab_issue(tile, reinterpret_cast<const float2*>(a.z) + (size_t)row0 * m, (int)min(32ll, a.npix - row0), m, S,
+                  lane);
+  cp_async_wait_all();
+  __syncwarp();
+  const long long i = row0 + lane;
+  if (i >= a.npix) return;
+  pixel_body<K, M, MODE>(a, i, true, tile + lane * S, s_hh, s_wh);
+}
+
+// K4: the harness update, elementwise over (pixel, k).
+template <int K>
+__global__ void __launch_bounds__(PX_THREADS) update_kernel(const PixArgs a) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.npix) return;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    float tn, an;
+    update_one(a, a.t_in[i * K + k], a.a_in[i * K + k], a.grad_t[i * K + k], a.grad_a[i * K + k], tn, an);
+    a.t_out[i * K + k] = tn;
+    a.a_out[i * K + k] = an;
+  }
+}
+
+static int px_num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int K, int M, int MODE>
 static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
-  const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
-  const size_t smem = MODE == PX_UPDATE ? 0 : sizeof(float2) * (PX_THREADS / 32) * 32 * zstride(M ? M : (int)a.m);
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set && MODE != PX_UPDATE) {
-    cudaError_t e = cudaFuncSetAttribute(pixel_kernel<K, M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(float2) * (PX_THREADS / 32) * 32 * zstride(MAX_M)));
+  if (MODE == PX_UPDATE) {
+    const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
+    update_kernel<K><<<(unsigned)grid, PX_THREADS, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  const int S = zstride(M ? M : (int)a.m);
+  const int warps = PX_THREADS / 32;
+  if (MODE == PX_EXPECTED) {
+    const size_t smem = sizeof(float2) * warps * 32 * S;
+    static bool attr_set = false;  // benign race: idempotent
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(expected_kernel<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(float2) * warps * 32 * zstride(MAX_M)));
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
+    expected_kernel<K, M><<<(unsigned)grid, PX_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  auto fn = grad_kernel<K, M, MODE>;
+  const size_t smem = sizeof(float2) * warps * 32 * S;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(float2) * warps * 32 * zstride(MAX_M)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  pixel_kernel<K, M, MODE><<<(unsigned)grid, PX_THREADS, smem, s>>>(a);
+  const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
+  fn<<<(unsigned)grid, PX_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 

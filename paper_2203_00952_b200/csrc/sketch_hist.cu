@@ -1,0 +1,174 @@
+// K5 — bin-count sketch path for pixels with many
+// photons (n >~ T):  Eq. (3) regrouped by time bin,
+//
+//   z_j = (1/n) sum_{x=0}^{T-1} h[x] exp(i 2 pi j x / T),   h[x] = #{p : x_p = x}
+//
+// which is the same sum in a different order (counts are exact integers), so
+// the result matches the direct path to rounding.  One
+// persistent CTA per pixel at a time:
+//   1. zero a shared uint32 histogram of T bins;
+//   2. stream the pixel's photons with 16-byte vector loads (4 in flight per
+//      thread) and count them with shared-memory atomics — 2 B of HBM per
+//      photon, no FP32 work: this is the HBM-bound phase;
+//   3. DFT of the histogram: thread t takes bins x = t, t+B, ..., weight
+//      h[x] * tab[x], then the packed complex recurrence over j (T*M terms per
+//      pixel instead of n*M);
+//   4. fixed-order block reduction (warp reduce-scatter + smem), scale by 1/n.
+#include <cstdint>
+
+#include "sketch_impl.cuh"
+
+namespace srt3d {
+
+constexpr int HS_THREADS = 512;
+
+template <int M>
+__global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
+  constexpr int NWARP = HS_THREADS / 32;
+  constexpr int NV = 2 * M;
+  constexpr int NVP = ((NV + 31) / 32) * 32;
+  constexpr int VL = NVP / 32;
+  extern __shared__ float2 tab[];
+  const uint32_t T = a.T, j0 = a.j0;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(tab + T + 1);
+  float* red = reinterpret_cast<float*>(hist + ((T + 3) & ~3u));
+  build_phase_table(tab, T);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float invT = 1.0f / (float)T;
+  const uint32_t off0 = (uint32_t)(((uintptr_t)a.bins >> 1) & 7u);
+  const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(a.bins - off0);
+  const uint16_t* __restrict__ bins = a.bins;
+
+  for (long long pix = blockIdx.x; pix < a.npix; pix += gridDim.x) {
+    for (uint32_t x = tid; x < T; x += HS_THREADS) hist[x] = 0u;
+    __syncthreads();  // (also orders the table build before first use)
+    unsigned long long beg = a.offsets[pix], end = a.offsets[pix + 1];
+    if (end < beg) end = beg;
+    const unsigned long long asb = (beg + off0 + 7u) & ~7ull;
+    const unsigned long long ase = (end + off0) & ~7ull;
+    unsigned long long hend = end, tbeg = end;
+    long long cb = 0, ce = 0;
+    if (asb < ase) {
+      hend = asb - off0;
+      tbeg = ase - off0;
+      cb = (long long)(asb >> 3);
+      ce = (long long)(ase >> 3);
+    }
+    const int nh = (int)(hend - beg), nt = (int)(end - tbeg);
+    if (tid < nh) atomicAdd(&hist[bins[beg + tid]], 1u);
+    else if (tid < nh + nt) atomicAdd(&hist[bins[tbeg + (tid - nh)]], 1u);
+    // body: 16-byte chunks, 4 loads in flight per thread
+    long long c = cb + tid;
+    for (; c + 3 * HS_THREADS < ce; c += 4 * HS_THREADS) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = __ldcs(vb + c + u * HS_THREADS);  // streamed once: evict-first
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+          atomicAdd(&hist[w4[h] & 0xffffu], 1u);
+          atomicAdd(&hist[w4[h] >> 16], 1u);
+        }
+      }
+    }
+    for (; c < ce; c += HS_THREADS) {
+      const uint4 v = __ldcs(vb + c);
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        atomicAdd(&hist[w4[h] & 0xffffu], 1u);
+        atomicAdd(&hist[w4[h] >> 16], 1u);
+      }
+    }
+    __syncthreads();
+
+    // DFT of the histogram over this thread's bins
+    u64 acc[M];
+#pragma unroll
+    for (int j = 0; j < M; j++) acc[j] = 0ull;
+    for (uint32_t x = tid; x < T; x += HS_THREADS) {
+      const float h = (float)hist[x];
+      const float2 w = tab[x];
+      const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
+      u64 P = W;
+      if (j0) {
+        const float2 an = tab[mod_small((j0 + 1) * x, T, invT)];
+        P = pk(an.x, an.y);
+      }
+      P = fmul2(pk(h, h), P);
+      acc[0] = fadd2(acc[0], P);
+#pragma unroll
+      for (int j = 1; j < M; j++) {
+        P = cmul2(P, W, Wn);
+        acc[j] = fadd2(acc[j], P);
+      }
+    }
+    float f[NVP];
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+      f[2 * j] = lo_of(acc[j]);
+      f[2 * j + 1] = hi_of(acc[j]);
+    }
+#pragma unroll
+    for (int i = NV; i < NVP; i++) f[i] = 0.f;
+    group_reduce_scatter<NVP, 32>(f, lane);
+#pragma unroll
+    for (int i = 0; i < VL; i++) red[warp * NVP + lane * VL + i] = f[i];
+    __syncthreads();
+    if (tid < NV) {
+      float sum = 0.f;
+#pragma unroll 4
+      for (int w = 0; w < NWARP; w++) sum += red[w * NVP + tid];
+      const unsigned long long n = end - beg;
+      const float inv = n ? 1.0f / (float)n : 0.0f;
+      a.z[((size_t)pix * a.mstride + j0) * 2 + tid] = sum * inv;
+    }
+    __syncthreads();  // red / hist reuse
+  }
+}
+
+size_t sketch_hist_smem(uint32_t T, int M) {
+  const int NVP = ((2 * M + 31) / 32) * 32;
+  return sizeof(float2) * (T + 1) + sizeof(uint32_t) * ((T + 3) & ~3u) + sizeof(float) * (HS_THREADS / 32) * NVP;
+}
+
+template <int M>
+static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
+  auto fn = sketch_hist_kernel<M>;
+  const size_t smem = sketch_hist_smem(a.T, M);
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, HS_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  long long grid = (long long)per_sm * num_sms;
+  if (grid > a.npix) grid = a.npix;
+  if (grid < 1) grid = 1;
+  fn<<<(unsigned)grid, HS_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sketch_hist(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
+  switch (M) {
+#define SRT3D_CASE(MM) \
+  case MM:             \
+    return launch_hist_t<MM>(a, s, num_sms);
+    SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
+    SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
+    SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)
+    SRT3D_CASE(23) SRT3D_CASE(24) SRT3D_CASE(25) SRT3D_CASE(26) SRT3D_CASE(27) SRT3D_CASE(28) SRT3D_CASE(29)
+    SRT3D_CASE(30) SRT3D_CASE(31) SRT3D_CASE(32)
+#undef SRT3D_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace srt3d

@@ -92,6 +92,53 @@ def test_sketch_regimes_by_hint(gpu, oracle_mod, inputs_mod):
         _assert_sketch_close(_host(z), zo)
 
 
+@pytest.mark.parametrize("T,m,max_n", [(4096, 10, 20000), (2500, 20, 12000), (1024, 4, 3000), (8192, 32, 9000),
+                                       (8192, 40, 9000), (100, 7, 500), (17000, 3, 40000)])
+def test_sketch_bincount_path_parity(gpu, oracle_mod, inputs_mod, T, m, max_n):
+    """NEXT-1 bin-count path (forced) vs the oracle, and vs the direct path, on ragged frames with
+    empty pixels and heavy pixels (n >> T)."""
+    import torch
+
+    bins, offs = inputs_mod.random_csr(npix=300, T=T, max_n=max_n, seed=T + m)
+    db, do = _dev(bins), _dev(offs)
+    zb = gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_BINCOUNT)
+    zd = gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_DIRECT)
+    torch.cuda.synchronize()
+    zo = oracle_mod.sketch(bins, offs, T, m)
+    _assert_sketch_close(_host(zb), zo)
+    _assert_sketch_close(_host(zd), zo)
+    assert np.all(_host(zb)[np.diff(offs.astype(np.int64)) == 0] == 0)
+
+
+def test_sketch_bincount_concentrated_signal(gpu, oracle_mod, inputs_mod):
+    """All photons of a pixel in a few bins (atomic contention) and SBR = inf."""
+    import torch
+
+    T = 4096
+    t = np.array([[5.0], [4090.5], [2048.0]], dtype=np.float32)
+    bins, offs = inputs_mod.sample_photons(t, np.array([[0.0, 1.0]] * 3), 0.5, T, seed=9, fixed_n=200000)
+    db, do = _dev(bins), _dev(offs)
+    zb = gpu.srt3d_sketch_ex(db, do, T, 10, total_photons=int(offs[-1]), path=gpu.PATH_BINCOUNT)
+    torch.cuda.synchronize()
+    _assert_sketch_close(_host(zb), oracle_mod.sketch(bins, offs, T, 10))
+
+
+def test_sketch_lane_regimes_forced(gpu, oracle_mod, inputs_mod):
+    import torch
+
+    bins, offs = inputs_mod.random_csr(npix=400, T=8192, max_n=1500, seed=21)
+    zo = oracle_mod.sketch(bins, offs, 8192, 32)
+    db, do = _dev(bins), _dev(offs)
+    for g in (4, 8, 16, 32):
+        z = gpu.srt3d_sketch_ex(db, do, 8192, 32, total_photons=int(offs[-1]), path=gpu.PATH_DIRECT, lanes_per_pixel=g)
+        torch.cuda.synchronize()
+        _assert_sketch_close(_host(z), zo)
+    with pytest.raises(gpu.Srt3dError):
+        gpu.srt3d_sketch_ex(db, do, 8192, 32, path=gpu.PATH_DIRECT, lanes_per_pixel=3)
+    with pytest.raises(gpu.Srt3dError):
+        gpu.srt3d_sketch_ex(db, do, 8192, 32, path=7)
+
+
 def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):
     """Segments starting at every residue mod 8, n = 0..17, non-zero offsets[0], odd bins base."""
     import torch
@@ -315,7 +362,7 @@ def _sample_idx(npix, k, seed):
 
 
 @pytest.mark.parametrize("name,n", [("C1", None), ("C2", None), ("C3", None), ("C5", None),
-                                    ("C4", 100), ("C4", 1000), ("C4", 10000), ("C4", 100000)])
+                                    ("C4", 100), ("C4", 1000), ("C4", 10000), ("C4", 100000), ("C4", 1000000)])
 def test_config_parity_full_size(gpu, oracle_mod, inputs_mod, name, n):
     """Full-size BASELINE configs, in the launch configuration bench.py uses (hinted regime):
     sketch checked on sampled pixels against the oracle; gradient at theta0 on sampled pixels."""
