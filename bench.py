@@ -329,43 +329,58 @@ def run_srt3d(args):
     fp32_peak = nsm * FP32_LANES_PER_SM * 2 * sm_max * 1e6  # flop/s at max clock
     sk_avg = statistics.mean(sk_ms)
     it_avg = statistics.mean(it_ms)
-    # sketch: F = 8 m n flops, B = 2n + 4 npix + 8 m npix bytes
-    sk_flops = 8.0 * f.m * f.n_photons
+    peak_src_fp32 = f"FP32: {nsm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (max clock; unit-count derivation)"
+    peak_src_hbm = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"
+
+    def roofline(kernel, bytes_, flops, ms):
+        """t_roof = max(bytes / HBM peak, flops / FP32 peak); frac = t_roof / t_measured."""
+        t_hbm, t_fp32 = bytes_ / (hbm * 1e9), flops / fp32_peak
+        t = ms * 1e-3
+        if t_hbm >= t_fp32:
+            return {"kernel": kernel, "bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": t_hbm / t, "peak_source": peak_src_hbm, "alg_bytes_per_launch": bytes_,
+                    "alg_flops_per_launch": flops}
+        return {"kernel": kernel, "bound": "alu", "achieved": flops / t / 1e12, "peak": fp32_peak / 1e12,
+                "unit": "TFLOP/s", "frac": t_fp32 / t, "peak_source": peak_src_fp32, "alg_bytes_per_launch": bytes_,
+                "alg_flops_per_launch": flops}
+
+    # sketch: B = 2n + 4(npix+1) + 8 m npix bytes; F = 8 m n (direct) or 8 m T npix (bin-count) (SURVEY §8(d))
+    path, lanes = srt3d.srt3d_sketch_plan(f.npix, f.T, f.m, f.n_photons)
     sk_bytes = 2.0 * f.n_photons + 4.0 * (f.npix + 1) + 8.0 * f.m * f.npix
-    sketch = {"kernel": "srt3d_sketch", "ms": sk_avg, "photons_per_s": f.n_photons / (sk_avg * 1e-3),
-              "gbs": sk_bytes / (sk_avg * 1e-3) / 1e9, "tflops": sk_flops / (sk_avg * 1e-3) / 1e12,
-              "frac_fp32": (sk_flops / (sk_avg * 1e-3)) / fp32_peak,
-              "frac_hbm": (sk_bytes / (sk_avg * 1e-3) / 1e9) / hbm}
+    sk_flops = 8.0 * f.m * (f.n_photons if path == srt3d.PATH_DIRECT else f.T * f.npix)
+    sketch = {"kernel": "srt3d_sketch", "path": "direct" if path == srt3d.PATH_DIRECT else "bincount",
+              "lanes_per_pixel": lanes, "ms": sk_avg, "photons_per_s": f.n_photons / (sk_avg * 1e-3),
+              "gbs": sk_bytes / (sk_avg * 1e-3) / 1e9, "frac_hbm": (sk_bytes / (sk_avg * 1e-3) / 1e9) / hbm,
+              "tflops_direct_count": 8.0 * f.m * f.n_photons / (sk_avg * 1e-3) / 1e12,
+              "roofline": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_avg)}
     grad = None
     if f.iters > 0:
         per_iter = it_avg / f.iters
         # fused step per pixel-iteration: read z (8m) + t, alpha (8K); write t, alpha (8K)
         g_bytes = f.npix * (8.0 * f.m + 16.0 * f.K) if pipe.fused else f.npix * (8.0 * f.m + 32.0 * f.K + 16.0 * f.K)
         g_flops = f.npix * (21.0 * f.K * f.m + 7.0 * f.m + 3.0 * f.K)
-        grad = {"kernel": "srt3d_sketch_grad_step" if pipe.fused else "srt3d_sketch_grad+srt3d_descent_update",
-                "ms_per_iter": per_iter, "pixel_iters_per_s": f.npix / (per_iter * 1e-3),
-                "gbs": g_bytes / (per_iter * 1e-3) / 1e9, "frac_hbm": g_bytes / (per_iter * 1e-3) / 1e9 / hbm,
-                "tflops": g_flops / (per_iter * 1e-3) / 1e12,
-                "frac_fp32": g_flops / (per_iter * 1e-3) / fp32_peak,
-                "note": "per-iteration time includes graph-node launch gaps; z stays L2-resident across iterations",
+        kname = "srt3d_sketch_grad_step" if pipe.fused else "srt3d_sketch_grad+srt3d_descent_update"
+        grad = {"kernel": kname, "ms_per_iter": per_iter, "pixel_iters_per_s": f.npix / (per_iter * 1e-3),
+                "gbs": g_bytes / (per_iter * 1e-3) / 1e9, "tflops": g_flops / (per_iter * 1e-3) / 1e12,
+                "roofline": roofline(kname, g_bytes, g_flops, per_iter),
+                "note": "in-loop (CUDA-graph) time per iteration incl. node launch gaps; z/theta stay L2-resident "
+                        "across iterations, so algorithmic bytes / time can exceed the HBM copy peak",
                 "cold_l2_ms_per_launch": grad_cold_ms,
-                "cold_l2_gbs": g_bytes / (grad_cold_ms * 1e-3) / 1e9 if grad_cold_ms else None,
-                "cold_l2_frac_hbm": g_bytes / (grad_cold_ms * 1e-3) / 1e9 / hbm if grad_cold_ms else None}
-    # dominant kernel -> roofline object
-    traffic = None
+                "cold_l2_roofline": roofline(kname, g_bytes, g_flops, grad_cold_ms) if grad_cold_ms else None}
+    # dominant kernel (larger share of the step) -> the line's roofline object
+    traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get(f.name, {})
     if grad is None or sk_avg >= it_avg:
-        roof = {"kernel": "srt3d_sketch", "bound": "alu", "achieved": sketch["tflops"], "peak": fp32_peak / 1e12,
-                "unit": "TFLOP/s", "frac": sketch["frac_fp32"],
-                "peak_source": f"FP32: {nsm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (max clock)",
-                "traffic": (traffic or {}).get("srt3d_sketch")}
+        roof = dict(sketch["roofline"])
+        roof["traffic"] = traffic.get("srt3d_sketch")
+        roof["share_of_step"] = sk_avg / (sk_avg + it_avg)
     else:
-        roof = {"kernel": grad["kernel"], "bound": "hbm", "achieved": grad["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": grad["frac_hbm"], "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "traffic": (traffic or {}).get("srt3d_sketch_grad_step")}
+        roof = dict(grad["roofline"])
+        roof["traffic"] = traffic.get("srt3d_sketch_grad_step")
+        roof["share_of_step"] = it_avg / (sk_avg + it_avg)
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

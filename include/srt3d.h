@@ -102,6 +102,15 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
                     uint64_t total_photons_hint, int path, int lanes_per_pixel, void* stream);
 
 /*
+ * srt3d_sketch_plan — host-only query: the path (SRT3D_PATH_DIRECT or
+ * SRT3D_PATH_BINCOUNT) and lanes per pixel srt3d_sketch would use for a frame
+ * of npix pixels and total_photons photons.  Returns the path (> 0) or a
+ * negative error code; *lanes_per_pixel (may be NULL) receives the lane count
+ * (0 for the bin-count path, which uses one CTA per pixel).
+ */
+int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photons, int* lanes_per_pixel);
+
+/*
  * srt3d_expected_sketch — Eq. (4) at omega_j = 2*pi*j/T with
  * the Gaussian IRF hhat(w) = exp(-sigma^2 w^2 / 2) (BASELINE.json north_star):
  *     z[i][j-1] = sum_{k<K} alpha[i][k] * hhat(omega_j) * exp(i omega_j t[i][k]).

@@ -179,13 +179,116 @@ __global__ void k_lds(float* out, float b, float c, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc.x + acc.y;
   if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
 }
+
+// mixed: 8 packed FFMA2 chains + 8 scalar FFMA chains per thread (can heavy+lite run concurrently?)
+__global__ void k_mix_ffma2_ffma(float* out, float b, float c, int iters) {
+  u64 a[NCH]; float s[NCH];
+  for (int i = 0; i < NCH; i++) { a[i] = pk(threadIdx.x * 1e-3f + i, i * 0.5f); s[i] = threadIdx.x * 1e-3f - i; }
+  u64 bb = pk(b + threadIdx.x * 1e-9f, b), cc = pk(c, c - threadIdx.x * 1e-9f);
+  float sb = b - threadIdx.x * 1e-9f, sc = c + threadIdx.x * 1e-9f;
+  __syncthreads(); u64 t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+#pragma unroll
+      for (int i = 0; i < NCH; i++) { a[i] = ffma2(a[i], bb, cc); s[i] = fmaf(s[i], sb, sc); }
+  }
+  __syncthreads(); u64 t1 = clock64();
+  float r = 0; for (int i = 0; i < NCH; i++) { float2 v = upk(a[i]); r += v.x + v.y + s[i]; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+// mixed: 2 packed FFMA2 per 1 scalar FFMA
+__global__ void k_mix_2ffma2_1ffma(float* out, float b, float c, int iters) {
+  u64 a[NCH]; float s[NCH];
+  for (int i = 0; i < NCH; i++) { a[i] = pk(threadIdx.x * 1e-3f + i, i * 0.5f); s[i] = threadIdx.x * 1e-3f - i; }
+  u64 bb = pk(b + threadIdx.x * 1e-9f, b), cc = pk(c, c - threadIdx.x * 1e-9f);
+  float sb = b - threadIdx.x * 1e-9f, sc = c + threadIdx.x * 1e-9f;
+  __syncthreads(); u64 t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+#pragma unroll
+      for (int i = 0; i < NCH; i++) { a[i] = ffma2(a[i], bb, cc); if (i & 1) s[i] = fmaf(s[i], sb, sc); }
+  }
+  __syncthreads(); u64 t1 = clock64();
+  float r = 0; for (int i = 0; i < NCH; i++) { float2 v = upk(a[i]); r += v.x + v.y + s[i]; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+// mixed FADD2 + scalar FFMA
+__global__ void k_mix_fadd2_ffma(float* out, float b, float c, int iters) {
+  u64 a[NCH]; float s[NCH];
+  for (int i = 0; i < NCH; i++) { a[i] = pk(threadIdx.x * 1e-3f + i, i * 0.5f); s[i] = threadIdx.x * 1e-3f - i; }
+  u64 bb = pk(b + threadIdx.x * 1e-9f, b);
+  float sb = b - threadIdx.x * 1e-9f, sc = c + threadIdx.x * 1e-9f;
+  __syncthreads(); u64 t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+#pragma unroll
+      for (int i = 0; i < NCH; i++) { a[i] = fadd2(a[i], bb); s[i] = fmaf(s[i], sb, sc); }
+  }
+  __syncthreads(); u64 t1 = clock64();
+  float r = 0; for (int i = 0; i < NCH; i++) { float2 v = upk(a[i]); r += v.x + v.y + s[i]; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+// scalar complex recurrence with scalar accumulate, 2 photon chains (ILP2), sketch-like
+template <int M>
+__global__ void k_cplx1x2(float* out, float b, float c, int iters) {
+  float Sr[M], Si[M]; for (int j = 0; j < M; j++) { Sr[j] = 0; Si[j] = 0; }
+  float wr = cosf(threadIdx.x * 1e-3f), wi = sinf(threadIdx.x * 1e-3f);
+  float vr = cosf(threadIdx.x * 2e-3f), vi = sinf(threadIdx.x * 2e-3f);
+  __syncthreads(); u64 t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+    float pr = wr, pi = wi, qr = vr, qi = vi;
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+      Sr[j] += pr + qr; Si[j] += pi + qi;
+      float nr = fmaf(pr, wr, -pi * wi); float ni = fmaf(pr, wi, pi * wr);
+      float mr = fmaf(qr, vr, -qi * vi); float mi = fmaf(qr, vi, qi * vr);
+      pr = nr; pi = ni; qr = mr; qi = mi;
+    }
+    wr += 1e-7f; wi -= 1e-7f; vr -= 1e-7f; vi += 1e-7f;
+  }
+  __syncthreads(); u64 t1 = clock64();
+  float s = 0; for (int j = 0; j < M; j++) s += Sr[j] + Si[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+// packed recurrence (FMUL2+FFMA2) but scalar accumulation FADD (lite pipe?), 2 chains
+template <int M>
+__global__ void k_cplx2_acc1(float* out, float b, float c, int iters) {
+  float Sr[M], Si[M]; for (int j = 0; j < M; j++) { Sr[j] = 0; Si[j] = 0; }
+  float wr = cosf(threadIdx.x * 1e-3f), wi = sinf(threadIdx.x * 1e-3f);
+  float vr = cosf(threadIdx.x * 2e-3f), vi = sinf(threadIdx.x * 2e-3f);
+  u64 W = pk(wr, wi), Wn = pk(-wi, wr), V = pk(vr, vi), Vn = pk(-vi, vr);
+  __syncthreads(); u64 t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+    u64 p = W, q = V;
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+      float2 pv = upk(p), qv = upk(q);
+      Sr[j] += pv.x; Si[j] += pv.y; Sr[j] += qv.x; Si[j] += qv.y;
+      p = ffma2(pk(pv.y, pv.y), Wn, fmul2(pk(pv.x, pv.x), W));
+      q = ffma2(pk(qv.y, qv.y), Vn, fmul2(pk(qv.x, qv.x), V));
+    }
+    W = fadd2(W, pk(1e-7f, -1e-7f)); Wn = pk(-upk(W).y, upk(W).x);
+    V = fadd2(V, pk(-1e-7f, 1e-7f)); Vn = pk(-upk(V).y, upk(V).x);
+  }
+  __syncthreads(); u64 t1 = clock64();
+  float s = 0; for (int j = 0; j < M; j++) s += Sr[j] + Si[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
 __global__ void k_copy(const uint4* __restrict__ a, uint4* __restrict__ b, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
 typedef void (*kfn)(float*, float, float, int);
-static void run(const char* name, kfn f, int iters, double lane_ops_per_iter_per_thread, int nsm, float* out) {
-  dim3 grid(nsm), block(1024);
+static void run(const char* name, kfn f, int iters, double lane_ops_per_iter_per_thread, int nsm, float* out, int bs = 1024) {
+  dim3 grid(nsm * (1024 / bs)), block(bs);
   f<<<grid, block>>>(out, 1.0000001f, 1e-7f, 8);  // warm
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -194,10 +297,11 @@ static void run(const char* name, kfn f, int iters, double lane_ops_per_iter_per
   cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   static unsigned long long cyc[4096];
-  CK(cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(u64) * nsm));
-  double mx = 0, mean = 0; for (int i = 0; i < nsm; i++) { mean += cyc[i]; if (cyc[i] > mx) mx = cyc[i]; }
-  mean /= nsm;
-  double ops = lane_ops_per_iter_per_thread * iters * 1024.0;  // per SM
+  int nb = nsm * (1024 / bs);
+  CK(cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(u64) * nb));
+  double mx = 0, mean = 0; for (int i = 0; i < nb; i++) { mean += cyc[i]; if (cyc[i] > mx) mx = cyc[i]; }
+  mean /= nb;
+  double ops = lane_ops_per_iter_per_thread * iters * 1024.0;  // per SM (all blocks resident)
   double per_clk = ops / mean;
   double clk_ghz = mx / (ms * 1e6);
   double total = ops * nsm / (ms * 1e-3);
@@ -217,9 +321,16 @@ int main() {
   run("fadd2_packed", k_fadd2, IT, 16.0 * NCH * 2, nsm, out);
   run("mufu_sin_cos", k_mufu, IT, NCH * 2.0, nsm, out);         // MUFU ops
   // sketch loops: report TERMS (photon x frequency) per clk per SM
-  run("sketch_cplx2_m32_terms", k_cplx2<32>, IT / 4, 32.0, nsm, out);
-  run("sketch_cplx1_m32_terms", k_cplx1<32>, IT / 4, 32.0, nsm, out);
-  run("sketch_cheb2_m32_terms", k_cheb2<32>, IT / 4, 32.0, nsm, out);
+  run("sketch_cplx2_m32_terms", k_cplx2<32>, IT / 4, 32.0, nsm, out, 256);
+  run("sketch_cplx1_m32_terms", k_cplx1<32>, IT / 4, 32.0, nsm, out, 256);
+  run("sketch_cheb2_m32_terms", k_cheb2<32>, IT / 4, 32.0, nsm, out, 256);
+  run("sketch_cplx1x2_m32_terms", k_cplx1x2<32>, IT / 4, 64.0, nsm, out, 256);
+  run("sketch_cplx2acc1_m32_terms", k_cplx2_acc1<32>, IT / 4, 64.0, nsm, out, 256);
+  run("sketch_cplx1x2_m16_terms", k_cplx1x2<16>, IT / 2, 32.0, nsm, out, 512);
+  run("sketch_cplx2acc1_m16_terms", k_cplx2_acc1<16>, IT / 2, 32.0, nsm, out, 512);
+  run("mix_ffma2_ffma", k_mix_ffma2_ffma, IT, 16.0 * NCH * 3, nsm, out);
+  run("mix_2ffma2_1ffma", k_mix_2ffma2_1ffma, IT, 16.0 * NCH * 2.5, nsm, out);
+  run("mix_fadd2_ffma", k_mix_fadd2_ffma, IT, 16.0 * NCH * 3, nsm, out);
   run("sketch_cplx2_m10_terms", k_cplx2<10>, IT, 10.0, nsm, out);
   run("sketch_cheb2_m10_terms", k_cheb2<10>, IT, 10.0, nsm, out);
   run("lds64_random", k_lds, IT, NCH, nsm, out);

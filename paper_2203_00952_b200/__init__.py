@@ -35,7 +35,8 @@ ERRORS = {-1: "SRT3D_EINVAL", -2: "SRT3D_ENULL", -3: "SRT3D_EUNSUPPORTED", -4: "
 PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT = 0, 1, 2
 EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
            "srt3d_sketch_grad",
-           "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index")
+           "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
+           "srt3d_sketch_plan")
 
 
 class Srt3dError(RuntimeError):
@@ -67,6 +68,7 @@ def load_library(path: str | None = None):
     lib.srt3d_sketch_grad_step.argtypes = [P, P, P, i64, u32, f32, u32, u32, f32, P, P]
     lib.srt3d_check_csr.argtypes = [P, P, i64, u32, P, P]
     lib.srt3d_debug_phase_index.argtypes = [P, i64, u32, u32, P, P]
+    lib.srt3d_sketch_plan.argtypes = [i64, u32, u32, u64, P]
     for f in EXPORTS[2:]:
         getattr(lib, f).restype = ctypes.c_int
     if path is None:
@@ -209,6 +211,16 @@ def fit_frame(bins, offsets, t0, alpha0, sigma: float, T: int, m: int, iters: in
             srt3d_sketch_grad(z, t, alpha, sigma, T, m, grad_t=gt, grad_alpha=ga, want_loss=False, stream=stream)
             srt3d_descent_update(t, alpha, gt, ga, sigma, T, m, eta, stream=stream)
     return z, t, alpha
+
+
+def srt3d_sketch_plan(npix: int, T: int, m: int, total_photons: int):
+    """(path, lanes_per_pixel) that srt3d_sketch uses for this frame shape (host-only query)."""
+    lanes = ctypes.c_int(0)
+    lib = load_library()
+    rc = lib.srt3d_sketch_plan(int(npix), int(T), int(m), int(total_photons), ctypes.byref(lanes))
+    if rc < 0:
+        raise Srt3dError(rc, lib.srt3d_last_error().decode())
+    return rc, lanes.value
 
 
 def version() -> int:

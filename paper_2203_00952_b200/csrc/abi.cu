@@ -86,11 +86,21 @@ void fill_consts(srt3d::PixArgs& a, float sigma, uint32_t T, uint32_t m, float e
 }
 
 int lanes_for(double mean_photons) {
-  // >= ~32 photons per lane amortises the group reduce-scatter
-  if (mean_photons >= 1024.0) return 32;
-  if (mean_photons >= 512.0) return 16;
+  // >= ~100 photons per lane amortises the group reduce-scatter and the
+  // head/tail peel (tools/sketch_tune.cu: G=8 beats G=16 at n=1000, m=32)
+  if (mean_photons >= 4096.0) return 32;
+  if (mean_photons >= 2048.0) return 16;
   if (mean_photons >= 256.0) return 8;
   return 4;
+}
+
+int choose_path(uint32_t T, uint32_t m, double mean, int* lanes) {
+  const int M0 = (int)(m < 32 ? m : 32);
+  const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
+  const int path = (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) ? SRT3D_PATH_BINCOUNT
+                                                                                        : SRT3D_PATH_DIRECT;
+  if (lanes) *lanes = path == SRT3D_PATH_BINCOUNT ? 0 : lanes_for(mean);
+  return path;
 }
 
 }  // namespace
@@ -131,9 +141,7 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   }
   if (!bins && total != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
   const double mean = (double)total / (double)npix;
-  if (path == SRT3D_PATH_AUTO)
-    path = (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) ? SRT3D_PATH_BINCOUNT
-                                                                                : SRT3D_PATH_DIRECT;
+  if (path == SRT3D_PATH_AUTO) path = choose_path(T, m, mean, nullptr);
   const int G = lanes_per_pixel ? lanes_per_pixel : lanes_for(mean);
   const int nsm = num_sms_current();
   srt3d::SketchArgs a;
@@ -151,6 +159,13 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
     if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
   }
   return SRT3D_OK;
+}
+
+int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photons, int* lanes_per_pixel) {
+  if (npix <= 0) return fail(SRT3D_EINVAL, "npix=%lld must be > 0", (long long)npix);
+  int rc = check_tm(T, m);
+  if (rc) return rc;
+  return choose_path(T, m, (double)total_photons / (double)npix, lanes_per_pixel);
 }
 
 int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,

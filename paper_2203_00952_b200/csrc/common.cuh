@@ -48,9 +48,20 @@ __device__ __forceinline__ u64 cmul2(u64 p, u64 W, u64 Wn) {
 }
 
 // ---- exact integer phase index (PAPER.md:61 with omega_j = 2 pi j / T) -----
-// r = (j * x) mod T for x < T <= 65536, j <= 64: j*x < 2^22, exact in uint32.
-__device__ __forceinline__ uint32_t phase_index(uint32_t x, uint32_t j, uint32_t T) {
-  return (j * x) % T;
+// (n mod T) for n < 2^23 without an integer division: fp32 quotient estimate
+// (n is exact in fp32, q is off by at most one) corrected by one step.
+__device__ __forceinline__ uint32_t mod_small(uint32_t n, uint32_t T, float invT) {
+  uint32_t q = __float2uint_rz(__uint2float_rz(n) * invT);
+  int r = (int)n - (int)(q * T);
+  if (r < 0) r += (int)T;
+  if (r >= (int)T) r -= (int)T;
+  return (uint32_t)r;
+}
+// r = (j * x) mod T for x < T <= 65536, j <= 64 (j*x < 2^22): the index of
+// exp(i omega_j x) in the exact phase table.  Used by every sketch path for
+// its anchors and by srt3d_debug_phase_index (bit-exactness test).
+__device__ __forceinline__ uint32_t phase_index(uint32_t x, uint32_t j, uint32_t T, float invT) {
+  return mod_small(j * x, T, invT);
 }
 
 // ---- fixed-point phase of a real depth (expected sketch / gradient) --------

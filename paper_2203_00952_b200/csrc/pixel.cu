@@ -102,16 +102,20 @@ __device__ __forceinline__ void update_one(const PixArgs& a, float tk, float ak,
 // pixel's z row in the shared tile (row stride S).  `active` lanes store;
 // inactive lanes (past the end of the frame) compute a duplicate and store
 // nothing (PX_EXPECTED writes its tile row, copied out by the caller).
-template <int K, int M, int MODE>
-__device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool active, float2* zrow,
-                                           const float* s_hh, const float* s_wh) {
-  const int m = M ? M : (int)a.m;
-  float tk[K], ak[K];
+template <int K>
+__device__ __forceinline__ void load_theta(const PixArgs& a, long long i, float (&tk)[K], float (&ak)[K]) {
 #pragma unroll
   for (int k = 0; k < K; k++) {
     tk[k] = a.t_in[i * K + k];
     ak[k] = a.a_in[i * K + k];
   }
+}
+
+template <int K, int M, int MODE>
+__device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool active, float2* zrow,
+                                           const float* s_hh, const float* s_wh, const float (&tk)[K],
+                                           const float (&ak)[K]) {
+  const int m = M ? M : (int)a.m;
   uint32_t q[K];
   u64 W[K], Wn[K], P[K];
 #pragma unroll
@@ -123,7 +127,12 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool a
     P[k] = W[k];
   }
 
-  float L = 0.f;
+  if (MODE != PX_EXPECTED) {
+    // the anchors above overlap the z slab's cp.async; wait for it only now
+    cp_async_wait_all();
+    __syncwarp();
+  }
+  u64 L2 = 0ull;  // packed (sum r_r^2, sum r_i^2)
   u64 GA[K], GT[K];  // packed partial sums: GA = sum (rho_r p_r, rho_i p_i); GT = sum (s_r p_i, -s_i p_r)
 #pragma unroll
   for (int k = 0; k < K; k++) {
@@ -162,11 +171,11 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool a
     } else {
       zj = zrow[j];
     }
-    const float rr = fmaf(-hh, lo_of(Sk), zj.x);
-    const float ri = fmaf(-hh, hi_of(Sk), zj.y);
-    L = fmaf(rr, rr, fmaf(ri, ri, L));
-    const u64 RHO = pk(hh * rr, hh * ri);   // hhat_j r_j
-    const u64 SIG = pk(wh * rr, -wh * ri);  // omega_j hhat_j (r_r, -r_i)
+    // packed: R = z_j - hh Sk ; L2 += R*R ; RHO = hh R ; SIG = (wh, -wh) * R
+    const u64 R = ffma2(pk(-hh, -hh), Sk, pk(zj.x, zj.y));
+    L2 = ffma2(R, R, L2);
+    const u64 RHO = fmul2(pk(hh, hh), R);   // hhat_j r_j
+    const u64 SIG = fmul2(pk(wh, -wh), R);  // omega_j hhat_j (r_r, -r_i)
 #pragma unroll
     for (int k = 0; k < K; k++) {
       GA[k] = ffma2(RHO, P[k], GA[k]);                          // (rho_r p_r, rho_i p_i)
@@ -181,7 +190,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool a
     ga[k] = -2.f * (lo_of(GA[k]) + hi_of(GA[k]));
     gt[k] = 2.f * ak[k] * (lo_of(GT[k]) + hi_of(GT[k]));
   }
-  if (a.loss) a.loss[i] = L;
+  if (a.loss) a.loss[i] = lo_of(L2) + hi_of(L2);
   if (MODE == PX_GRAD) {
 #pragma unroll
     for (int k = 0; k < K; k++) {
@@ -227,7 +236,9 @@ __global__ void __launch_bounds__(PX_THREADS) expected_kernel(const PixArgs a) {
   const int S = zstride(m);
   float2* tile = ztile + (size_t)warp * 32 * S;
   const bool active = i < a.npix;
-  pixel_body<K, M, PX_EXPECTED>(a, active ? i : a.npix - 1, active, tile + lane * S, s_hh, s_wh);
+  float tk[K], ak[K];
+  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
+  pixel_body<K, M, PX_EXPECTED>(a, active ? i : a.npix - 1, active, tile + lane * S, s_hh, s_wh, tk, ak);
   __syncwarp();
   warp_slab_store(tile, reinterpret_cast<float2*>(a.zout) + (size_t)row0 * m, nrows, m, S, lane);
 }
@@ -247,11 +258,13 @@ __global__ void __launch_bounds__(PX_THREADS) grad_kernel(const PixArgs a) {
   float2* tile = ztile + (size_t)warp * 32 * S;
   warp_slab_issue(tile, reinterpret_cast<const float2*>(a.z) + (size_t)row0 * m, (int)min(32ll, a.npix - row0), m, S,
                   lane);
-  cp_async_wait_all();
-  __syncwarp();
   const long long i = row0 + lane;
-  if (i >= a.npix) return;
-  pixel_body<K, M, MODE>(a, i, true, tile + lane * S, s_hh, s_wh);
+  const bool active = i < a.npix;
+  float tk[K], ak[K];
+  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);  // in flight together with the z slab
+  // inactive lanes (past the frame end) run a duplicate of the last pixel so
+  // the warp stays converged at the in-body cp.async wait; they store nothing
+  pixel_body<K, M, MODE>(a, active ? i : a.npix - 1, active, tile + lane * S, s_hh, s_wh, tk, ak);
 }
 
 // K4: the harness update, elementwise over (pixel, k).

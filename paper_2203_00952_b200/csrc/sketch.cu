@@ -14,9 +14,10 @@ cudaError_t launch_sketch_g32(int M, bool tab, const SketchArgs& a, cudaStream_t
 // ---- debug / validation kernels -----------------------------------------
 __global__ void phase_index_kernel(const uint16_t* __restrict__ bins, long long n, uint32_t T, uint32_t m,
                                    uint32_t* __restrict__ r) {
+  const float invT = 1.0f / (float)T;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
     const uint32_t x = bins[p];
-    for (uint32_t j = 1; j <= m; j++) r[(size_t)p * m + (j - 1)] = phase_index(x, j, T);
+    for (uint32_t j = 1; j <= m; j++) r[(size_t)p * m + (j - 1)] = phase_index(x, j, T, invT);
   }
 }
 

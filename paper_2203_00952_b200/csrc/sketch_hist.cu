@@ -7,7 +7,7 @@
 // the result matches the direct path to rounding.  One
 // persistent CTA per pixel at a time:
 //   1. zero a shared uint32 histogram of T bins;
-//   2. stream the pixel's photons with 16-byte vector loads (4 in flight per
+//   2. stream the pixel's photons with 16-byte vector loads (8 in flight per
 //      thread) and count them with shared-memory atomics — 2 B of HBM per
 //      photon, no FP32 work: this is the HBM-bound phase;
 //   3. DFT of the histogram: thread t takes bins x = t, t+B, ..., weight
@@ -20,9 +20,12 @@
 
 namespace srt3d {
 
-constexpr int HS_THREADS = 512;
+#ifndef HS_DEFAULT_THREADS
+#define HS_DEFAULT_THREADS 512  // CTA size (tools/hist_tune.cu)
+#define HS_DEFAULT_UNROLL 8     // 16-byte loads in flight per thread
+#endif
 
-template <int M>
+template <int M, int HS_THREADS, int HS_UNROLL>
 __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
   constexpr int NWARP = HS_THREADS / 32;
   constexpr int NV = 2 * M;
@@ -39,9 +42,9 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(a.bins - off0);
   const uint16_t* __restrict__ bins = a.bins;
 
+  for (uint32_t x = tid; x < T; x += HS_THREADS) hist[x] = 0u;  // later re-zeroed by the DFT pass
   for (long long pix = blockIdx.x; pix < a.npix; pix += gridDim.x) {
-    for (uint32_t x = tid; x < T; x += HS_THREADS) hist[x] = 0u;
-    __syncthreads();  // (also orders the table build before first use)
+    __syncthreads();  // table build / previous pixel's DFT (which re-zeroes hist) done
     unsigned long long beg = a.offsets[pix], end = a.offsets[pix + 1];
     if (end < beg) end = beg;
     const unsigned long long asb = (beg + off0 + 7u) & ~7ull;
@@ -57,14 +60,14 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
     const int nh = (int)(hend - beg), nt = (int)(end - tbeg);
     if (tid < nh) atomicAdd(&hist[bins[beg + tid]], 1u);
     else if (tid < nh + nt) atomicAdd(&hist[bins[tbeg + (tid - nh)]], 1u);
-    // body: 16-byte chunks, 4 loads in flight per thread
+    // body: 16-byte chunks, HS_UNROLL loads in flight per thread
     long long c = cb + tid;
-    for (; c + 3 * HS_THREADS < ce; c += 4 * HS_THREADS) {
-      uint4 v[4];
+    for (; c + (HS_UNROLL - 1) * HS_THREADS < ce; c += HS_UNROLL * HS_THREADS) {
+      uint4 v[HS_UNROLL];
 #pragma unroll
-      for (int u = 0; u < 4; u++) v[u] = __ldcs(vb + c + u * HS_THREADS);  // streamed once: evict-first
+      for (int u = 0; u < HS_UNROLL; u++) v[u] = __ldcs(vb + c + u * HS_THREADS);  // streamed once: evict-first
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < HS_UNROLL; u++) {
         const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int h = 0; h < 4; h++) {
@@ -90,11 +93,12 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
     for (int j = 0; j < M; j++) acc[j] = 0ull;
     for (uint32_t x = tid; x < T; x += HS_THREADS) {
       const float h = (float)hist[x];
+      hist[x] = 0u;  // ready for the next pixel
       const float2 w = tab[x];
       const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
       u64 P = W;
       if (j0) {
-        const float2 an = tab[mod_small((j0 + 1) * x, T, invT)];
+        const float2 an = tab[phase_index(x, j0 + 1, T, invT)];
         P = pk(an.x, an.y);
       }
       P = fmul2(pk(h, h), P);
@@ -129,15 +133,15 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
   }
 }
 
-size_t sketch_hist_smem(uint32_t T, int M) {
+inline size_t sketch_hist_smem_t(uint32_t T, int M, int nthreads) {
   const int NVP = ((2 * M + 31) / 32) * 32;
-  return sizeof(float2) * (T + 1) + sizeof(uint32_t) * ((T + 3) & ~3u) + sizeof(float) * (HS_THREADS / 32) * NVP;
+  return sizeof(float2) * (T + 1) + sizeof(uint32_t) * ((T + 3) & ~3u) + sizeof(float) * (nthreads / 32) * NVP;
 }
 
-template <int M>
+template <int M, int HS_THREADS = HS_DEFAULT_THREADS, int HS_UNROLL = HS_DEFAULT_UNROLL>
 static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
-  auto fn = sketch_hist_kernel<M>;
-  const size_t smem = sketch_hist_smem(a.T, M);
+  auto fn = sketch_hist_kernel<M, HS_THREADS, HS_UNROLL>;
+  const size_t smem = sketch_hist_smem_t(a.T, M, HS_THREADS);
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -155,6 +159,9 @@ static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sm
   return cudaGetLastError();
 }
 
+#ifndef HS_NO_DISPATCH
+size_t sketch_hist_smem(uint32_t T, int M) { return sketch_hist_smem_t(T, M, 512); }  // largest CTA variant
+
 cudaError_t launch_sketch_hist(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
   switch (M) {
 #define SRT3D_CASE(MM) \
@@ -170,5 +177,6 @@ cudaError_t launch_sketch_hist(int M, const SketchArgs& a, cudaStream_t s, int n
       return cudaErrorInvalidValue;
   }
 }
+#endif
 
 }  // namespace srt3d

@@ -53,16 +53,6 @@ __device__ __forceinline__ float2 phasor_exact(uint32_t r, uint32_t T) {
   return make_float2((float)cs, (float)sn);
 }
 
-// (n mod T) for n < 2^23 without an integer division: fp32 quotient estimate
-// (n exact in fp32) corrected by at most one step either way.
-__device__ __forceinline__ uint32_t mod_small(uint32_t n, uint32_t T, float invT) {
-  uint32_t q = __float2uint_rz(__uint2float_rz(n) * invT);
-  int r = (int)n - (int)(q * T);
-  if (r < 0) r += (int)T;
-  if (r >= (int)T) r -= (int)T;
-  return (uint32_t)r;
-}
-
 // Per-lane accumulators of one pass (M frequencies) over a pixel's photons.
 // TP = table period: with TP > 0 every TP-th term is read from the exact
 // phase table (index advanced by d = TP*x mod T on the ALU pipe) instead of
@@ -94,8 +84,8 @@ struct PhotonAcc {
       const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x), V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
       u64 P = W, Q = V;
       if (j0) {
-        const float2 pa = phasor_exact(phase_index(x, j0 + 1, T), T);
-        float2 qa = phasor_exact(phase_index(y, j0 + 1, T), T);
+        const float2 pa = phasor_exact(phase_index(x, j0 + 1, T, invT), T);
+        float2 qa = phasor_exact(phase_index(y, j0 + 1, T, invT), T);
         if (!yvalid) qa = make_float2(0.f, 0.f);
         P = pk(pa.x, pa.y);
         Q = pk(qa.x, qa.y);
@@ -116,8 +106,8 @@ struct PhotonAcc {
     uint32_t rx = x * 8u, ry = yy * 8u;
     u64 P = W, Q = V;
     if (j0) {
-      rx = mod_small((j0 + 1) * x, T, invT) * 8u;
-      ry = yvalid ? mod_small((j0 + 1) * y, T, invT) * 8u : T * 8u;
+      rx = phase_index(x, j0 + 1, T, invT) * 8u;
+      ry = yvalid ? phase_index(y, j0 + 1, T, invT) * 8u : T * 8u;
       P = lds64(tab, rx);
       Q = lds64(tab, ry);
     }
