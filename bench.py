@@ -294,16 +294,18 @@ def run_srt3d(args):
                "ms_per_step": float(e2e_ms.item()) / args.e2e_steps}
 
     # L2-cold per-launch time of the gradient kernel (outside the timed region):
-    # flush L2 (write 2x its size) before each launch, CUDA events around it.
+    # flush L2 by READING a buffer of 2x its size (leaves clean lines: no
+    # write-back traffic lands on the timed kernel), CUDA events around it.
     grad_cold_ms = None
     if f.iters > 0:
         l2 = torch.cuda.get_device_properties(local).L2_cache_size
-        flush = torch.empty(2 * max(l2, 1 << 20) // 4, dtype=torch.float32, device="cuda")
+        flush = torch.ones(2 * max(l2, 1 << 20) // 4, dtype=torch.float32, device="cuda")
+        sink = torch.empty(1, dtype=torch.float32, device="cuda")
         tt, aa = pipe.t0.clone(), pipe.a0.clone()
         times = []
         with torch.cuda.stream(s):
             for r in range(6):
-                flush.fill_(float(r))
+                torch.sum(flush, dim=0, out=sink[0])
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
                 if pipe.fused:

@@ -163,6 +163,18 @@ int srt3d_sketch_grad_step(const float* z, float* t, float* alpha, int64_t npix,
                            uint32_t m, float eta, float* loss, void* stream);
 
 /*
+ * srt3d_fit_pixelwise — `iters` fused data steps in ONE launch (SURVEY §8(f)
+ * NEXT-2, the pixelwise sketched fit of Eq. (6), with no
+ * spatial coupling between iterations): z is staged once, t/alpha stay in
+ * registers, and every iteration is exactly the srt3d_sketch_grad_step
+ * arithmetic (the result equals `iters` srt3d_sketch_grad_step calls).
+ * t and alpha are updated in place.  loss (optional, float [npix]) receives
+ * the loss at the returned parameters.  iters <= 2^24.
+ */
+int srt3d_fit_pixelwise(const float* z, float* t, float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
+                        uint32_t m, float eta, uint32_t iters, float* loss, void* stream);
+
+/*
  * srt3d_check_csr — debug validator (not on the hot path).  Sets *bad (a
  * device int32 the caller zeroes first) to non-zero if some bins[p] >= T or
  * some offsets[i+1] < offsets[i].

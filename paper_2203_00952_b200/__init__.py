@@ -36,7 +36,7 @@ PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT = 0, 1, 2
 EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
            "srt3d_sketch_grad",
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
-           "srt3d_sketch_plan")
+           "srt3d_sketch_plan", "srt3d_fit_pixelwise")
 
 
 class Srt3dError(RuntimeError):
@@ -69,6 +69,7 @@ def load_library(path: str | None = None):
     lib.srt3d_check_csr.argtypes = [P, P, i64, u32, P, P]
     lib.srt3d_debug_phase_index.argtypes = [P, i64, u32, u32, P, P]
     lib.srt3d_sketch_plan.argtypes = [i64, u32, u32, u64, P]
+    lib.srt3d_fit_pixelwise.argtypes = [P, P, P, i64, u32, f32, u32, u32, f32, u32, P, P]
     for f in EXPORTS[2:]:
         getattr(lib, f).restype = ctypes.c_int
     if path is None:
@@ -167,6 +168,16 @@ def srt3d_sketch_grad_step(z, t, alpha, sigma: float, T: int, m: int, eta: float
     npix, K = t.shape
     _need_cuda(z, t, alpha, loss)
     _call("srt3d_sketch_grad_step", _ptr(z), _ptr(t), _ptr(alpha), npix, K, float(sigma), T, m, float(eta),
+          _ptr(loss), _stream(stream))
+    return t, alpha
+
+
+def srt3d_fit_pixelwise(z, t, alpha, sigma: float, T: int, m: int, iters: int, eta: float = 0.5, loss=None,
+                        stream=None):
+    """NEXT-2: `iters` fused data steps in one launch (t, alpha updated in place)."""
+    npix, K = t.shape
+    _need_cuda(z, t, alpha, loss)
+    _call("srt3d_fit_pixelwise", _ptr(z), _ptr(t), _ptr(alpha), npix, K, float(sigma), T, m, float(eta), int(iters),
           _ptr(loss), _stream(stream))
     return t, alpha
 

@@ -79,6 +79,7 @@ void fill_consts(srt3d::PixArgs& a, float sigma, uint32_t T, uint32_t m, float e
   a.m = m;
   a.invT = 1.0 / (double)T;
   a.Tf = (float)T;
+  a.invTf = (float)(1.0 / (double)T);
   a.eta = eta;
   a.upd_t_scale = (float)(1.0 / (2.0 * sw2h2));
   a.upd_a_scale = (float)(1.0 / (2.0 * sh2));
@@ -258,6 +259,30 @@ int srt3d_sketch_grad_step(const float* z, float* t, float* alpha, int64_t npix,
   a.npix = npix;
   cudaError_t e = srt3d::launch_pixel(srt3d::PX_GRAD_STEP, (int)K, a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch_grad_step");
+  return SRT3D_OK;
+}
+
+int srt3d_fit_pixelwise(const float* z, float* t, float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
+                        uint32_t m, float eta, uint32_t iters, float* loss, void* stream) {
+  int rc = check_kparams(npix, K, sigma, T, m);
+  if (rc) return rc;
+  if (!std::isfinite(eta) || eta <= 0.f) return fail(SRT3D_EINVAL, "eta=%g must be finite and > 0", (double)eta);
+  if (iters > (1u << 24)) return fail(SRT3D_EINVAL, "iters=%u too large", iters);
+  if (npix == 0 || (iters == 0 && !loss)) return SRT3D_OK;
+  if (!z || !t || !alpha) return fail(SRT3D_ENULL, "z/t/alpha must be non-NULL");
+  if (!aligned(z, 8) || !aligned(t, 4) || !aligned(alpha, 4) || (loss && !aligned(loss, 4)))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and t/alpha/loss 4-byte aligned");
+  srt3d::PixArgs a = {};
+  fill_consts(a, sigma, T, m, eta);
+  a.z = z;
+  a.t_in = t;
+  a.a_in = alpha;
+  a.t_out = t;
+  a.a_out = alpha;
+  a.loss = loss;
+  a.npix = npix;
+  cudaError_t e = srt3d::launch_fit((int)K, a, (int)iters, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_fit_pixelwise");
   return SRT3D_OK;
 }
 

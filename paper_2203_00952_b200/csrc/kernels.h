@@ -11,6 +11,9 @@ constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T < 24576 
 #define SK_TABLE_PERIOD 0                        // every TP-th sketch term read from the table (0 = off)
 #endif
 constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
+#ifndef GRAD_THREADS
+#define GRAD_THREADS 64                          // gradient-kernel CTA size (one warp = 32 pixels)
+#endif
 constexpr int MAX_M = 64;
 constexpr int MAX_K = 8;
 
@@ -50,6 +53,7 @@ struct PixArgs {
   float upd_a_scale;  // 1 / (2 * sum_j hhat_j^2)
   float max_step;     // T / (4 m)
   float Tf;
+  float invTf;        // 1 / T (fp32)
   FreqConsts c;
 };
 
@@ -63,5 +67,6 @@ cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, ui
 cudaError_t launch_check_csr(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,
                              int32_t* bad, cudaStream_t s, int num_sms);
 cudaError_t launch_pixel(PixMode mode, int K, const PixArgs& a, cudaStream_t s);
+cudaError_t launch_fit(int K, const PixArgs& a, int iters, cudaStream_t s);
 
 }  // namespace srt3d

@@ -88,14 +88,16 @@ __device__ __forceinline__ void warp_slab_store(const float2* tile, float2* gdst
 // step and K4 so both produce bit-identical results.
 __device__ __forceinline__ void update_one(const PixArgs& a, float tk, float ak, float gt, float ga, float& tn,
                                            float& an) {
+  // branch-free: approximate reciprocal division (harness update, not part of
+  // the paper's arithmetic; the oracle comparison tolerance covers ~2 ulp)
   const float am = fmaxf(ak, 0.05f);
-  float step = a.eta * gt * a.upd_t_scale / (am * am);
+  float step = __fdividef(a.eta * gt * a.upd_t_scale, am * am);
   step = fminf(fmaxf(step, -a.max_step), a.max_step);
   tn = tk - step;
-  tn = tn - a.Tf * floorf(tn / a.Tf);
-  if (tn >= a.Tf) tn -= a.Tf;
-  if (tn < 0.f) tn += a.Tf;
-  an = fminf(fmaxf(ak - a.eta * ga * a.upd_a_scale, 0.f), 1.f);
+  tn = fmaf(-a.Tf, floorf(tn * a.invTf), tn);
+  tn = tn >= a.Tf ? tn - a.Tf : tn;
+  tn = tn < 0.f ? tn + a.Tf : tn;
+  an = fminf(fmaxf(fmaf(-a.eta * a.upd_a_scale, ga, ak), 0.f), 1.f);
 }
 
 // One pixel: anchors, the j loop, and the mode's outputs.  zrow points at the
@@ -111,10 +113,13 @@ __device__ __forceinline__ void load_theta(const PixArgs& a, long long i, float 
   }
 }
 
-template <int K, int M, int MODE>
-__device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool active, float2* zrow,
-                                           const float* s_hh, const float* s_wh, const float (&tk)[K],
-                                           const float (&ak)[K]) {
+// Evaluates one pixel: Phi (PX_EXPECTED: written to zrow), else the loss L and
+// the gradient (gt, ga).  WAIT_Z: wait for the warp's cp.async z slab after
+// the anchors (which overlap the copy).
+template <int K, int M, int MODE, bool WAIT_Z = true>
+__device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const float* s_hh, const float* s_wh,
+                                           const float (&tk)[K], const float (&ak)[K], float (&gt)[K],
+                                           float (&ga)[K], float& L) {
   const int m = M ? M : (int)a.m;
   uint32_t q[K];
   u64 W[K], Wn[K], P[K];
@@ -127,7 +132,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool a
     P[k] = W[k];
   }
 
-  if (MODE != PX_EXPECTED) {
+  if (MODE != PX_EXPECTED && WAIT_Z) {
     // the anchors above overlap the z slab's cp.async; wait for it only now
     cp_async_wait_all();
     __syncwarp();
@@ -182,15 +187,20 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, long long i, bool a
       GT[k] = ffma2(SIG, pk(hi_of(P[k]), lo_of(P[k])), GT[k]);  // (s_r p_i, -s_i p_r)
     }
   }
-  if (MODE == PX_EXPECTED || !active) return;
-
-  float gt[K], ga[K];
+  if (MODE == PX_EXPECTED) return;
 #pragma unroll
   for (int k = 0; k < K; k++) {
     ga[k] = -2.f * (lo_of(GA[k]) + hi_of(GA[k]));
     gt[k] = 2.f * ak[k] * (lo_of(GT[k]) + hi_of(GT[k]));
   }
-  if (a.loss) a.loss[i] = lo_of(L2) + hi_of(L2);
+  L = lo_of(L2) + hi_of(L2);
+}
+
+// Stores of one evaluated pixel, per mode (gradient / fused step).
+template <int K, int MODE>
+__device__ __forceinline__ void pixel_store(const PixArgs& a, long long i, const float (&tk)[K], const float (&ak)[K],
+                                            const float (&gt)[K], const float (&ga)[K], float L) {
+  if (a.loss) a.loss[i] = L;
   if (MODE == PX_GRAD) {
 #pragma unroll
     for (int k = 0; k < K; k++) {
@@ -238,7 +248,8 @@ __global__ void __launch_bounds__(PX_THREADS) expected_kernel(const PixArgs a) {
   const bool active = i < a.npix;
   float tk[K], ak[K];
   load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
-  pixel_body<K, M, PX_EXPECTED>(a, active ? i : a.npix - 1, active, tile + lane * S, s_hh, s_wh, tk, ak);
+  float gt[K], ga[K], L;
+  pixel_body<K, M, PX_EXPECTED>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
   __syncwarp();
   warp_slab_store(tile, reinterpret_cast<float2*>(a.zout) + (size_t)row0 * m, nrows, m, S, lane);
 }
@@ -246,7 +257,36 @@ __global__ void __launch_bounds__(PX_THREADS) expected_kernel(const PixArgs a) {
 // Gradient / fused step (K3, K3+K4): one warp = 32 pixels; the warp's z slab
 // is staged into its shared tile with cp.async, then each lane runs its pixel.
 template <int K, int M, int MODE>
-__global__ void __launch_bounds__(PX_THREADS) grad_kernel(const PixArgs a) {
+__global__ void __launch_bounds__(GRAD_THREADS) grad_kernel(const PixArgs a) {
+  __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
+  extern __shared__ float2 ztile[];
+  stage_consts<M>(a, s_hh, s_wh);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
+  if (row0 >= a.npix) return;
+  const int m = M ? M : (int)a.m;
+  const int S = zstride(m);
+  float2* tile = ztile + (size_t)warp * 32 * S;
+  const long long i = row0 + lane;
+  const bool active = i < a.npix;
+  float tk[K], ak[K];
+  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);  // first: the anchors need theta before z
+  warp_slab_issue(tile, reinterpret_cast<const float2*>(a.z) + (size_t)row0 * m, (int)min(32ll, a.npix - row0), m, S,
+                  lane);
+  // inactive lanes (past the frame end) run a duplicate of the last pixel so
+  // the warp stays converged at the in-body cp.async wait; they store nothing
+  float gt[K], ga[K], L;
+  pixel_body<K, M, MODE>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
+  if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
+}
+
+// NEXT-2: `iters` fused data steps per pixel in one launch.
+// The warp stages its z slab once; theta lives in registers across the
+// iterations (each iteration is exactly the PX_GRAD_STEP arithmetic, so the
+// result is bitwise equal to `iters` srt3d_sketch_grad_step calls).  If
+// loss != NULL, the loss at the returned theta is evaluated once more.
+template <int K, int M>
+__global__ void __launch_bounds__(GRAD_THREADS) fit_kernel(const PixArgs a, int iters) {
   __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
   extern __shared__ float2 ztile[];
   stage_consts<M>(a, s_hh, s_wh);
@@ -261,10 +301,90 @@ __global__ void __launch_bounds__(PX_THREADS) grad_kernel(const PixArgs a) {
   const long long i = row0 + lane;
   const bool active = i < a.npix;
   float tk[K], ak[K];
-  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);  // in flight together with the z slab
-  // inactive lanes (past the frame end) run a duplicate of the last pixel so
-  // the warp stays converged at the in-body cp.async wait; they store nothing
-  pixel_body<K, M, MODE>(a, active ? i : a.npix - 1, active, tile + lane * S, s_hh, s_wh, tk, ak);
+  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
+  cp_async_wait_all();
+  __syncwarp();
+  float gt[K], ga[K], L = 0.f;
+  for (int it = 0; it < iters; it++) {
+    pixel_body<K, M, PX_GRAD_STEP, false>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      float tn, an;
+      update_one(a, tk[k], ak[k], gt[k], ga[k], tn, an);
+      tk[k] = tn;
+      ak[k] = an;
+    }
+  }
+  if (a.loss) pixel_body<K, M, PX_GRAD, false>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    a.t_out[i * K + k] = tk[k];
+    a.a_out[i * K + k] = ak[k];
+  }
+  if (a.loss) a.loss[i] = L;
+}
+
+template <int K, int M>
+static cudaError_t launch_fit_t(const PixArgs& a, int iters, cudaStream_t s) {
+  auto fn = fit_kernel<K, M>;
+  const int S = zstride(M ? M : (int)a.m);
+  const size_t smem = sizeof(float2) * (GRAD_THREADS / 32) * 32 * S;
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(float2) * (GRAD_THREADS / 32) * 32 * zstride(MAX_M)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
+  fn<<<(unsigned)grid, GRAD_THREADS, smem, s>>>(a, iters);
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t launch_fit_m(const PixArgs& a, int iters, cudaStream_t s) {
+  if (K <= 3) {
+    switch (a.m) {
+      case 4:
+        return launch_fit_t<K, 4>(a, iters, s);
+      case 5:
+        return launch_fit_t<K, 5>(a, iters, s);
+      case 10:
+        return launch_fit_t<K, 10>(a, iters, s);
+      case 20:
+        return launch_fit_t<K, 20>(a, iters, s);
+      case 32:
+        return launch_fit_t<K, 32>(a, iters, s);
+      default:
+        break;
+    }
+  }
+  return launch_fit_t<K, 0>(a, iters, s);
+}
+
+cudaError_t launch_fit(int K, const PixArgs& a, int iters, cudaStream_t s) {
+  if (a.npix <= 0) return cudaSuccess;
+  switch (K) {
+    case 1:
+      return launch_fit_m<1>(a, iters, s);
+    case 2:
+      return launch_fit_m<2>(a, iters, s);
+    case 3:
+      return launch_fit_m<3>(a, iters, s);
+    case 4:
+      return launch_fit_m<4>(a, iters, s);
+    case 5:
+      return launch_fit_m<5>(a, iters, s);
+    case 6:
+      return launch_fit_m<6>(a, iters, s);
+    case 7:
+      return launch_fit_m<7>(a, iters, s);
+    case 8:
+      return launch_fit_m<8>(a, iters, s);
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 // K4: the harness update, elementwise over (pixel, k).
@@ -315,16 +435,17 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
     return cudaGetLastError();
   }
   auto fn = grad_kernel<K, M, MODE>;
-  const size_t smem = sizeof(float2) * warps * 32 * S;
+  const int gwarps = GRAD_THREADS / 32;
+  const size_t smem = sizeof(float2) * gwarps * 32 * S;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(float2) * warps * 32 * zstride(MAX_M)));
+                                         (int)(sizeof(float2) * gwarps * 32 * zstride(MAX_M)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
-  fn<<<(unsigned)grid, PX_THREADS, smem, s>>>(a);
+  const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
+  fn<<<(unsigned)grid, GRAD_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 

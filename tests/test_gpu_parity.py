@@ -336,6 +336,31 @@ def test_update_parity_and_fused_step(gpu, oracle_mod, inputs_mod):
     assert np.abs(_host(a1) - ao).max() <= 1e-6
 
 
+@pytest.mark.parametrize("T,m,sigma,K", [(8192, 32, 6.0, 3), (1024, 4, 2.0, 1), (2500, 20, 3.0, 2), (1000, 7, 1.0, 2),
+                                         (8192, 40, 6.0, 1)])
+def test_fit_pixelwise_equals_iterated_steps(gpu, oracle_mod, inputs_mod, T, m, sigma, K):
+    """NEXT-2: iters fused steps in one launch == iters srt3d_sketch_grad_step calls; loss = loss at result."""
+    import torch
+
+    npix = 1000
+    t, a = inputs_mod.random_theta(npix, K, T, seed=5, alpha_lo=0.05, alpha_hi=1.0)
+    zt = gpu.srt3d_expected_sketch(_dev(t), _dev(a), sigma, T, m)
+    t0 = (t + np.float32(3.0)).astype(np.float32)
+    t1, a1 = _dev(t0), _dev(a)
+    for _ in range(7):
+        gpu.srt3d_sketch_grad_step(zt, t1, a1, sigma, T, m, eta=0.5)
+    t2, a2 = _dev(t0), _dev(a)
+    loss = torch.empty(npix, device="cuda")
+    gpu.srt3d_fit_pixelwise(zt, t2, a2, sigma, T, m, iters=7, eta=0.5, loss=loss)
+    torch.cuda.synchronize()
+    assert torch.equal(t1, t2) and torch.equal(a1, a2)
+    gt, ga, L = gpu.srt3d_sketch_grad(zt, t2, a2, sigma, T, m)
+    torch.cuda.synchronize()
+    assert torch.equal(L, loss)
+    go = oracle_mod.sketch_grad(_host(zt), _host(t2), _host(a2), sigma, T, m)
+    _grad_tol_check(_host(zt), _host(t2), _host(a2), sigma, T, m, (_host(gt), _host(ga), _host(loss)), go)
+
+
 def test_iterations_reduce_loss_c1(gpu, oracle_mod, inputs_mod):
     """C1 end to end: sketch, then 20 iterations from t* + 10; loss falls and depths approach t*."""
     import torch
