@@ -349,8 +349,10 @@ def run_srt3d(args):
     # sketch: B = 2n + 4(npix+1) + 8 m npix bytes; F = 8 m n (direct) or 8 m T npix (bin-count)
     path, lanes = srt3d.srt3d_sketch_plan(f.npix, f.T, f.m, f.n_photons)
     sk_bytes = 2.0 * f.n_photons + 4.0 * (f.npix + 1) + 8.0 * f.m * f.npix
-    sk_flops = 8.0 * f.m * (f.n_photons if path == srt3d.PATH_DIRECT else f.T * f.npix)
-    sketch = {"kernel": "srt3d_sketch", "path": "direct" if path == srt3d.PATH_DIRECT else "bincount",
+    direct_sum = path in (srt3d.PATH_DIRECT, srt3d.PATH_PAIRED)
+    sk_flops = 8.0 * f.m * (f.n_photons if direct_sum else f.T * f.npix)
+    sketch = {"kernel": "srt3d_sketch",
+              "path": {srt3d.PATH_DIRECT: "direct", srt3d.PATH_PAIRED: "paired"}.get(path, "bincount"),
               "lanes_per_pixel": lanes, "ms": sk_avg, "photons_per_s": f.n_photons / (sk_avg * 1e-3),
               "gbs": sk_bytes / (sk_avg * 1e-3) / 1e9, "frac_hbm": (sk_bytes / (sk_avg * 1e-3) / 1e9) / hbm,
               "tflops_direct_count": 8.0 * f.m * f.n_photons / (sk_avg * 1e-3) / 1e12,

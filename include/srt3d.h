@@ -86,27 +86,35 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  * (same result up to fp32 rounding order; used by tests and tuning):
  *   path            SRT3D_PATH_AUTO (0): bin-count when the mean photon count
  *                   per pixel is >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * T and
- *                   the histogram fits in shared memory, else direct;
- *                   SRT3D_PATH_DIRECT (1): per-photon complex recurrence;
+ *                   the histogram fits in shared memory, else direct
+ *                   (AUTO never selects PAIRED: measured slower);
+ *                   SRT3D_PATH_DIRECT (1): per-photon complex recurrence,
+ *                   lanes_per_pixel lanes per pixel;
  *                   SRT3D_PATH_BINCOUNT (2): per-pixel shared-memory
  *                   histogram h[x] then z_j = (1/n) sum_x h[x] e^{i 2 pi j x/T}
  *                   (the same sum as Eq. (3) regrouped by bin; T <= ~17000,
- *                   else SRT3D_EUNSUPPORTED).
+ *                   else SRT3D_EUNSUPPORTED);
+ *                   SRT3D_PATH_PAIRED (3): the direct sum, one warp per pixel,
+ *                   photons sorted by phase class into (A, B) pairs that run
+ *                   the rotated Chebyshev recurrence (
+ *                   T < 24576, else SRT3D_EUNSUPPORTED).
  *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path only).
  */
 #define SRT3D_PATH_AUTO 0
 #define SRT3D_PATH_DIRECT 1
 #define SRT3D_PATH_BINCOUNT 2
+#define SRT3D_PATH_PAIRED 3
 #define SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN 1.0
 int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
                     uint64_t total_photons_hint, int path, int lanes_per_pixel, void* stream);
 
 /*
- * srt3d_sketch_plan — host-only query: the path (SRT3D_PATH_DIRECT or
- * SRT3D_PATH_BINCOUNT) and lanes per pixel srt3d_sketch would use for a frame
+ * srt3d_sketch_plan — host-only query: the path (SRT3D_PATH_DIRECT,
+ * SRT3D_PATH_BINCOUNT or SRT3D_PATH_PAIRED) and lanes per pixel srt3d_sketch would use for a frame
  * of npix pixels and total_photons photons.  Returns the path (> 0) or a
  * negative error code; *lanes_per_pixel (may be NULL) receives the lane count
- * (0 for the bin-count path, which uses one CTA per pixel).
+ * (0 for the bin-count path, which uses one CTA per pixel; 32 for the
+ * paired path, one warp per pixel).
  */
 int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photons, int* lanes_per_pixel);
 

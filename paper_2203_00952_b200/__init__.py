@@ -32,7 +32,7 @@ _lib = None
 
 SRT3D_OK = 0
 ERRORS = {-1: "SRT3D_EINVAL", -2: "SRT3D_ENULL", -3: "SRT3D_EUNSUPPORTED", -4: "SRT3D_ECUDA", -5: "SRT3D_EALIGN"}
-PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT = 0, 1, 2
+PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT, PATH_PAIRED = 0, 1, 2, 3
 EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
            "srt3d_sketch_grad",
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
@@ -116,7 +116,7 @@ def srt3d_sketch(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: t
 def srt3d_sketch_ex(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: torch.Tensor | None = None,
                     total_photons: int | None = None, path: int = PATH_AUTO, lanes_per_pixel: int = 0,
                     stream=None) -> torch.Tensor:
-    """Eq. (3) with the launch regime chosen explicitly (PATH_DIRECT / PATH_BINCOUNT, lanes 4..32)."""
+    """Eq. (3) with the launch regime chosen explicitly (PATH_DIRECT with lanes 4..32, PATH_BINCOUNT, PATH_PAIRED)."""
     npix = offsets.numel() - 1
     if z is None:
         z = torch.empty((max(npix, 0), m), dtype=torch.complex64, device=offsets.device)

@@ -95,12 +95,14 @@ int lanes_for(double mean_photons) {
   return 4;
 }
 
+bool pair_fits(uint32_t T) { return ((size_t)T + 1) * sizeof(float2) <= srt3d::SK_MAX_SMEM; }
+
 int choose_path(uint32_t T, uint32_t m, double mean, int* lanes) {
   const int M0 = (int)(m < 32 ? m : 32);
   const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
-  const int path = (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) ? SRT3D_PATH_BINCOUNT
-                                                                                        : SRT3D_PATH_DIRECT;
-  if (lanes) *lanes = path == SRT3D_PATH_BINCOUNT ? 0 : lanes_for(mean);
+  int path = SRT3D_PATH_DIRECT;
+  if (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) path = SRT3D_PATH_BINCOUNT;
+  if (lanes) *lanes = path == SRT3D_PATH_BINCOUNT ? 0 : (path == SRT3D_PATH_PAIRED ? 32 : lanes_for(mean));
   return path;
 }
 
@@ -117,7 +119,7 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
   int rc = check_tm(T, m);
   if (rc) return rc;
-  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_BINCOUNT) return fail(SRT3D_EINVAL, "path=%d unknown", path);
+  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_PAIRED) return fail(SRT3D_EINVAL, "path=%d unknown", path);
   if (lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 && lanes_per_pixel != 16 &&
       lanes_per_pixel != 32)
     return fail(SRT3D_EINVAL, "lanes_per_pixel=%d must be 0, 4, 8, 16 or 32", lanes_per_pixel);
@@ -130,6 +132,8 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
   if (path == SRT3D_PATH_BINCOUNT && !hist_fits)
     return fail(SRT3D_EUNSUPPORTED, "bin-count path needs T <= ~17000 (T=%u)", T);
+  if (path == SRT3D_PATH_PAIRED && !pair_fits(T))
+    return fail(SRT3D_EUNSUPPORTED, "paired path needs T < 24576 (T=%u)", T);
   cudaStream_t s = (cudaStream_t)stream;
   uint64_t total = total_photons_hint;
   if (total == 0 && (path == SRT3D_PATH_AUTO || lanes_per_pixel == 0)) {
@@ -156,6 +160,7 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
     a.j0 = j0;
     const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
     cudaError_t e = path == SRT3D_PATH_BINCOUNT ? srt3d::launch_sketch_hist(M, a, s, nsm)
+                    : path == SRT3D_PATH_PAIRED ? srt3d::launch_sketch_pair(M, a, s, nsm)
                                                 : srt3d::launch_sketch_pass(M, G, a, s, nsm);
     if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
   }

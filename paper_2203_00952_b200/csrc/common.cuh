@@ -41,6 +41,9 @@ __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
   return d;
 }
 
+// -v (ptxas folds the negation into the consuming FFMA2/FADD2 operand).
+__device__ __forceinline__ u64 neg2(u64 v) { return pk(-lo_of(v), -hi_of(v)); }
+
 // Complex multiply p * w with packed ops: (pr,pr)*(wr,wi) + (pi,pi)*(-wi,wr).
 // W = (wr, wi), Wn = (-wi, wr).  2 instructions, 4 FP32 lane-ops.
 __device__ __forceinline__ u64 cmul2(u64 p, u64 W, u64 Wn) {

@@ -7,8 +7,8 @@ namespace srt3d {
 
 constexpr int SK_THREADS = 256;                 // sketch CTA size
 constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T < 24576 uses the smem table)
-#ifndef SK_TABLE_PERIOD
-#define SK_TABLE_PERIOD 0                        // every TP-th sketch term read from the table (0 = off)
+#ifndef SK_SCHEME
+#define SK_SCHEME 0                              // grouped direct path phasor scheme: 0 complex power, 1 rotated Chebyshev (selects)
 #endif
 constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 #ifndef GRAD_THREADS
@@ -68,6 +68,8 @@ enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3 };
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_sketch_hist(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
 size_t sketch_hist_smem(uint32_t T, int M);
+cudaError_t launch_sketch_pair(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
+size_t sketch_pair_smem(uint32_t T);
 cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, uint32_t m, uint32_t* r,
                                cudaStream_t s, int num_sms);
 cudaError_t launch_check_csr(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,

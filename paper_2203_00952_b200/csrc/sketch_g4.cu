@@ -3,6 +3,6 @@
 
 namespace srt3d {
 cudaError_t launch_sketch_g4(int M, bool tab, const SketchArgs& a, cudaStream_t s, int num_sms) {
-  return dispatch_m<4, true, SK_TABLE_PERIOD>(M, a, s, num_sms);
+  return dispatch_m<4, true, SK_SCHEME>(M, a, s, num_sms);
 }
 }  // namespace srt3d

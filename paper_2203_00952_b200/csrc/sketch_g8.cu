@@ -3,6 +3,6 @@
 
 namespace srt3d {
 cudaError_t launch_sketch_g8(int M, bool tab, const SketchArgs& a, cudaStream_t s, int num_sms) {
-  return dispatch_m<8, true, SK_TABLE_PERIOD>(M, a, s, num_sms);
+  return dispatch_m<8, true, SK_SCHEME>(M, a, s, num_sms);
 }
 }  // namespace srt3d

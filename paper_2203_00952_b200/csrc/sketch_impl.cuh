@@ -23,6 +23,7 @@
 //    lane keeps 2M/G sums) into per-lane fp32 results.  The order is fixed,
 //    so results are bitwise reproducible.
 #include <cstdint>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -53,97 +54,149 @@ __device__ __forceinline__ float2 phasor_exact(uint32_t r, uint32_t T) {
   return make_float2((float)cs, (float)sn);
 }
 
+// Multiply by i^n (n taken mod 4): exact (component swap / negation).
+__device__ __forceinline__ float2 mul_ipow(float2 v, uint32_t n) {
+  switch (n & 3u) {
+    case 1: return make_float2(-v.y, v.x);
+    case 2: return make_float2(-v.x, -v.y);
+    case 3: return make_float2(v.y, -v.x);
+    default: return v;
+  }
+}
+
 // Per-lane accumulators of one pass (M frequencies) over a pixel's photons.
-// TP = table period: with TP > 0 every TP-th term is read from the exact
-// phase table (index advanced by d = TP*x mod T on the ALU pipe) instead of
-// one more complex multiply; this moves work off the FP32 pipe (FADD2 only)
-// and re-anchors the chain.  The table carries a zero entry at index T,
-// used as the "absent photon" (keeps one copy of the unrolled body).
-template <int M, bool TAB, int TP>
+//
+// SCH selects the phasor scheme for the terms j = j0+1 .. j0+M:
+//  * SCH_CPOW: complex-power recurrence p_j = p_{j-1} * w (FMUL2 + FFMA2 per
+//    term) + S_j += p_j (FADD2): 6 FP32 lane-ops per (photon, j).
+//  * SCH_CHEB: rotated Chebyshev recurrence.  Both components of
+//    v_j = e^{i j theta'} obey v_j = 2 cos(theta') v_{j-1} - v_{j-2}, one
+//    FFMA2 per term (scalar broadcast coefficient, negated operand folded).
+//    The recurrence is ill-conditioned where sin(theta') ~ 0 (the fp32
+//    coefficient's rounding becomes an angle error delta / sin theta'), so a
+//    photon whose base angle has |sin theta| < |cos theta| runs the chain on
+//    theta' = theta + pi/2 (exact: i * w), |sin theta'| >= 1/sqrt 2, and its
+//    terms are rotated back by (-i)^j — compile-time per j: nothing (j%4=0),
+//    a sign (j%4=2, folded into an FFMA2 with a +-1 broadcast), or a
+//    component swap with a sign (odd j: two selects on the ALU pipe).
+//    4 FP32 lane-ops per (photon, j).  Worst-case phasor error 1.4e-6 for
+//    j <= 32 and 2.8e-6 for j <= 64 at every T tested (tools/sim_cheb_error.c,
+//    the same fp32 FMA sequence run for every x < T), equal to SCH_CPOW's.
+// The table carries a zero entry at index T, used as the "absent photon"
+// (keeps one copy of the unrolled body).
+enum { SCH_CPOW = 0, SCH_CHEB = 1 };
+
+template <int M, bool TAB, int SCH>
 struct PhotonAcc {
   u64 acc[M];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = 0ull;
   }
-  __device__ __forceinline__ float2 base(const float2* tab, uint32_t r, uint32_t T) const {
+  __device__ __forceinline__ static float2 base(const float2* tab, uint32_t r, uint32_t T) {
     if (TAB) return tab[r];
+    if (r >= T) return make_float2(0.f, 0.f);
     return phasor_exact(r, T);
   }
-  __device__ __forceinline__ static u64 lds64(const float2* tab, uint32_t boff) {
-    const float2 v = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(tab) + boff);
-    return pk(v.x, v.y);
-  }
+
   // Two photons x, y as interleaved chains (ILP 2).  If !yvalid the second
-  // chain uses the zero table entry / w = 0 and contributes exactly 0.
+  // chain contributes exactly 0 (zero base phasor / zero seeds).
   __device__ __forceinline__ void add2(const float2* tab, uint32_t x, uint32_t y, bool yvalid, uint32_t T,
                                        uint32_t j0, float invT) {
-    if (!TAB) {
-      float2 w = phasor_exact(x, T), v = phasor_exact(y, T);
-      if (!yvalid) v = make_float2(0.f, 0.f);
-      const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x), V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
-      u64 P = W, Q = V;
-      if (j0) {
-        const float2 pa = phasor_exact(phase_index(x, j0 + 1, T, invT), T);
-        float2 qa = phasor_exact(phase_index(y, j0 + 1, T, invT), T);
-        if (!yvalid) qa = make_float2(0.f, 0.f);
-        P = pk(pa.x, pa.y);
-        Q = pk(qa.x, qa.y);
-      }
-      acc[0] = fadd2(acc[0], fadd2(P, Q));
-#pragma unroll
-      for (int j = 1; j < M; j++) {
-        P = cmul2(P, W, Wn);
-        Q = cmul2(Q, V, Vn);
-        acc[j] = fadd2(acc[j], fadd2(P, Q));
-      }
+    const uint32_t yy = yvalid ? y : T;  // tab[T] = 0
+    if (SCH != SCH_CPOW) {
+      add2_cheb(tab, x, yy, yvalid, T, j0, invT);
       return;
     }
-    const uint32_t yy = yvalid ? y : T;  // tab[T] = 0
-    const float2 w = tab[x], v = tab[yy];
+    const float2 w = base(tab, x, T), v = base(tab, yy, T);
     const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x), V = pk(v.x, v.y), Vn = pk(-v.y, v.x);
-    // byte offsets of the current anchor index r_j = (j x) mod T, and the TP step
-    uint32_t rx = x * 8u, ry = yy * 8u;
     u64 P = W, Q = V;
     if (j0) {
-      rx = phase_index(x, j0 + 1, T, invT) * 8u;
-      ry = yvalid ? phase_index(y, j0 + 1, T, invT) * 8u : T * 8u;
-      P = lds64(tab, rx);
-      Q = lds64(tab, ry);
-    }
-    uint32_t dx = 0, dy = 0, dxT = 0, dyT = 0;
-    if (TP > 0) {
-      dx = mod_small(TP * x, T, invT) * 8u;
-      dy = yvalid ? mod_small(TP * y, T, invT) * 8u : 0u;
-      dxT = dx - 8u * T;                  // r + d - T (mod 2^32)
-      dyT = yvalid ? dy - 8u * T : 0u;
-    }
-    // the next anchor is fetched one period ahead (hides the LDS latency)
-    u64 Pn = 0ull, Qn = 0ull;
-    if (TP > 0 && TP < M) {
-      rx = min(rx + dx, rx + dxT);  // unsigned: (r + d) mod T, scaled by 8
-      ry = min(ry + dy, ry + dyT);
-      Pn = lds64(tab, rx);
-      Qn = lds64(tab, ry);
+      const float2 pa = base(tab, phase_index(x, j0 + 1, T, invT), T);
+      const float2 qa = base(tab, yvalid ? phase_index(y, j0 + 1, T, invT) : T, T);
+      P = pk(pa.x, pa.y);
+      Q = pk(qa.x, qa.y);
     }
     acc[0] = fadd2(acc[0], fadd2(P, Q));
 #pragma unroll
     for (int j = 1; j < M; j++) {
-      if (TP > 0 && (j % TP) == 0) {
-        P = Pn;
-        Q = Qn;
-        if (j + TP < M) {
-          rx = min(rx + dx, rx + dxT);
-          ry = min(ry + dy, ry + dyT);
-          Pn = lds64(tab, rx);
-          Qn = lds64(tab, ry);
-        }
-      } else {
-        P = cmul2(P, W, Wn);
-        Q = cmul2(Q, V, Vn);
-      }
+      P = cmul2(P, W, Wn);
+      Q = cmul2(Q, V, Vn);
       acc[j] = fadd2(acc[j], fadd2(P, Q));
     }
+  }
+
+  // Per-photon constants of a rotated Chebyshev chain.
+  struct ChebLane {
+    u64 C2;  // (2 cos theta', 2 cos theta')
+    u64 G2;  // (g, g), g = -1 if rotated else +1
+    bool k;  // rotated by +pi/2
+  };
+  // Term J (0-based within the pass) of two chains: advance (J > 0) and
+  // accumulate, rotated back by (-i)^{1+J} for a rotated chain.  A
+  // compile-time index keeps the per-J code straight-line.
+  template <int J>
+  __device__ __forceinline__ void cheb_term(const ChebLane& X, const ChebLane& Y, u64& Ax, u64& Bx, u64& Ay,
+                                            u64& By) {
+    if constexpr (J > 0) {
+      const u64 Nx = ffma2(Bx, X.C2, neg2(Ax));
+      const u64 Ny = ffma2(By, Y.C2, neg2(Ay));
+      Ax = Bx;
+      Bx = Nx;
+      Ay = By;
+      By = Ny;
+    }
+    constexpr int rot = (1 + J) & 3;
+    if constexpr (rot == 0) {
+      acc[J] = fadd2(acc[J], fadd2(Bx, By));
+    } else if constexpr (rot == 2) {
+      acc[J] = ffma2(By, Y.G2, ffma2(Bx, X.G2, acc[J]));
+    } else {  // rot 1: (-i) v = (s, -c); rot 3: (+i) v = (-s, c)
+      constexpr float sg = rot == 1 ? 1.f : -1.f;
+      const float bxr = lo_of(Bx), bxi = hi_of(Bx), byr = lo_of(By), byi = hi_of(By);
+      const u64 Xr = pk(X.k ? sg * bxi : bxr, X.k ? -sg * bxr : bxi);
+      const u64 Yr = pk(Y.k ? sg * byi : byr, Y.k ? -sg * byr : byi);
+      acc[J] = fadd2(acc[J], fadd2(Xr, Yr));
+    }
+  }
+  template <int... J>
+  __device__ __forceinline__ void cheb_terms(std::integer_sequence<int, J...>, const ChebLane& X, const ChebLane& Y,
+                                             u64& Ax, u64& Bx, u64& Ay, u64& By) {
+    (cheb_term<J>(X, Y, Ax, Bx, Ay, By), ...);
+  }
+
+  // Rotated Chebyshev body (SCH_CHEB).  j0 must be a multiple of 4 (passes
+  // are 32 wide), so the back-rotation (-i)^j depends on j - j0 only.
+  __device__ __forceinline__ void add2_cheb(const float2* tab, uint32_t x, uint32_t yy, bool yvalid, uint32_t T,
+                                            uint32_t j0, float invT) {
+    const float2 w = base(tab, x, T), v = base(tab, yy, T);
+    // SCH 2 (tools/sketch_tune.cu only): no rotation — wrong near sin = 0, used
+    // to time the class-uniform body
+    const bool kx = SCH == 2 ? false : fabsf(w.y) < fabsf(w.x), ky = SCH == 2 ? false : fabsf(v.y) < fabsf(v.x);
+    // rotated bases e^{i theta'} = i^k w
+    const float cx = kx ? -w.y : w.x, sx = kx ? w.x : w.y;
+    const float cy = ky ? -v.y : v.x, sy = ky ? v.x : v.y;
+    const float Cx = 2.f * cx, Cy = 2.f * cy;
+    const float gx = kx ? -1.f : 1.f, gy = ky ? -1.f : 1.f;
+    // seeds: (A, B) = (v_{j0}, v_{j0+1}) of each rotated chain
+    u64 Ax, Bx, Ay, By;
+    if (j0 == 0) {
+      Ax = pk(1.f, 0.f);
+      Bx = pk(cx, sx);
+      Ay = pk(yvalid ? 1.f : 0.f, 0.f);
+      By = pk(cy, sy);
+    } else {
+      const float2 a0 = mul_ipow(base(tab, phase_index(x, j0, T, invT), T), kx ? j0 : 0u);
+      const float2 a1 = mul_ipow(base(tab, phase_index(x, j0 + 1, T, invT), T), kx ? j0 + 1 : 0u);
+      const float2 b0 = mul_ipow(base(tab, yvalid ? phase_index(yy, j0, T, invT) : T, T), ky ? j0 : 0u);
+      const float2 b1 = mul_ipow(base(tab, yvalid ? phase_index(yy, j0 + 1, T, invT) : T, T), ky ? j0 + 1 : 0u);
+      Ax = pk(a0.x, a0.y);
+      Bx = pk(a1.x, a1.y);
+      Ay = pk(b0.x, b0.y);
+      By = pk(b1.x, b1.y);
+    }
+    const ChebLane X{pk(Cx, Cx), pk(gx, gx), kx}, Y{pk(Cy, Cy), pk(gy, gy), ky};
+    cheb_terms(std::make_integer_sequence<int, M>{}, X, Y, Ax, Bx, Ay, By);
   }
 };
 
@@ -164,7 +217,7 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int gl) {
   }
 }
 
-template <int M, int G, bool TAB, int TP>
+template <int M, int G, bool TAB, int SCH>
 __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
   extern __shared__ float2 tab[];
   if (TAB) {
@@ -209,7 +262,7 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
       cb = (long long)(asb >> 3);
       ce = (long long)(ase >> 3);
     }
-    PhotonAcc<M, TAB, TP> pa;
+    PhotonAcc<M, TAB, SCH> pa;
     pa.zero();
     // scalar head + tail peel (< 8 photons each), processed in pairs through
     // the same add2 body as the vector loop
@@ -277,9 +330,9 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
 }
 
 // ---- host-side dispatch ---------------------------------------------------
-template <int M, int G, bool TAB, int TP>
+template <int M, int G, bool TAB, int SCH>
 static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
-  auto fn = sketch_kernel<M, G, TAB, TP>;
+  auto fn = sketch_kernel<M, G, TAB, SCH>;
   const size_t smem = TAB ? sizeof(float2) * (a.T + 1) : 0;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
@@ -301,12 +354,12 @@ static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_
   return cudaGetLastError();
 }
 
-template <int G, bool TAB, int TP>
+template <int G, bool TAB, int SCH>
 static cudaError_t dispatch_m(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
   switch (M) {
 #define SRT3D_CASE(MM) \
   case MM:             \
-    return launch_sketch_t<MM, G, TAB, TP>(a, s, num_sms);
+    return launch_sketch_t<MM, G, TAB, SCH>(a, s, num_sms);
     SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
     SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
     SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)

@@ -139,6 +139,65 @@ def test_sketch_lane_regimes_forced(gpu, oracle_mod, inputs_mod):
         gpu.srt3d_sketch_ex(db, do, 8192, 32, path=7)
 
 
+@pytest.mark.parametrize("T,m", [(8192, 32), (8192, 64), (4613, 10), (1024, 4), (2500, 20), (2, 1), (3, 2),
+                                 (17, 16), (24575, 33), (100, 7)])
+@pytest.mark.parametrize("max_n", [9, 300, 3000])
+def test_sketch_paired_path_parity(gpu, oracle_mod, inputs_mod, T, m, max_n):
+    """Paired path (one warp per pixel, class-sorted Chebyshev pairs) forced on ragged frames with
+    empty pixels, heads/tails of every length and pixels spanning many 256-photon rounds."""
+    import torch
+
+    bins, offs = inputs_mod.random_csr(npix=333, T=T, max_n=max_n, seed=T * 3 + m + max_n)
+    z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED)
+    torch.cuda.synchronize()
+    zg = _host(z)
+    _assert_sketch_close(zg, oracle_mod.sketch(bins, offs, T, m))
+    assert np.all(zg[np.diff(offs.astype(np.int64)) == 0] == 0)
+
+
+@pytest.mark.parametrize("T", [8192, 4613, 24575, 1024])
+def test_sketch_paired_worst_bins(gpu, oracle_mod, T):
+    """Every photon of a pixel at one bin (no averaging of phasor errors): the bins where the
+    unrotated recurrence is worst conditioned (0, 1, T/2 +- 1, T-1), the class boundaries
+    (4u = T, 3T), and one-class pixels larger than the queue (forced single-class steps)."""
+    import torch
+
+    u = [T // 8, (3 * T) // 8, (T + 7) // 8, T // 4]
+    xs = sorted({0, 1, 2, T - 1, T // 2, T // 2 + 1, T // 2 - 1, T // 4, (3 * T) // 4, *u, *(x + T // 2 for x in u)})
+    xs = [x % T for x in xs]
+    lists = [[x] * 3001 for x in xs]
+    lists.append(list(np.arange(2000) % 7))          # class A/B mix at tiny bins
+    lists.append([T // 4] * 1500 + [0] * 5)           # almost one class, then the other
+    bins, offs = _csr(lists)
+    for m in (32, 64):
+        z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, min(m, T - 1), total_photons=int(offs[-1]),
+                                path=gpu.PATH_PAIRED)
+        torch.cuda.synchronize()
+        _assert_sketch_close(_host(z), oracle_mod.sketch(bins, offs, T, min(m, T - 1)))
+
+
+def test_sketch_paired_alignment_and_determinism(gpu, oracle_mod, inputs_mod):
+    """Misaligned bins base, offsets[0] != 0, bitwise repeatability, T limit."""
+    import torch
+
+    T, m = 8192, 32
+    bins, offs = inputs_mod.random_csr(npix=257, T=T, max_n=2000, seed=77)
+    for shift in range(0, 8):
+        pad = np.concatenate([np.full(shift + 3, T - 1, np.uint16), bins])
+        full = _dev(pad)
+        sub = full[shift:]  # 2-byte aligned start at every residue mod 8
+        o = (offs + np.uint32(3)).astype(np.uint32)
+        z = gpu.srt3d_sketch_ex(sub, _dev(o), T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED)
+        torch.cuda.synchronize()
+        _assert_sketch_close(_host(z), oracle_mod.sketch(bins, offs, T, m))
+    db, do = _dev(bins), _dev(offs)
+    z1 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED))
+    z2 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED))
+    assert np.array_equal(z1.view(np.uint64), z2.view(np.uint64))
+    with pytest.raises(gpu.Srt3dError):
+        gpu.srt3d_sketch_ex(db, do, 30000, m, path=gpu.PATH_PAIRED)
+
+
 def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):
     """Segments starting at every residue mod 8, n = 0..17, non-zero offsets[0], odd bins base."""
     import torch
