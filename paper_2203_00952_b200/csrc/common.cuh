@@ -79,6 +79,9 @@ __device__ __forceinline__ uint32_t phase_q32(float t, double invT) {
 }
 // exp(i * 2 pi * q / 2^32) with q interpreted as a signed half-open
 // revolution in [-1/2, 1/2): sincospif on a = q * 2^-31 in [-1, 1).
+// (A 256-entry table + residual polynomial variant, tools/gen_phase_tab.py,
+// was as accurate but slower in the kernel: the dependent global table load
+// sits on the anchor's critical path.)
 __device__ __forceinline__ float2 phasor_q32(uint32_t q) {
   float a = (float)(int32_t)q * 4.656612873077392578125e-10f;  // 2^-31
   float s, c;

@@ -280,53 +280,6 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_MIN_BLOCKS) grad_kernel(con
   if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
 }
 
-// Persistent variant: each warp walks 32-pixel tiles; theta of the next tile
-// is prefetched into registers during the current tile, and the next z slab
-// is issued into the (single) tile buffer as soon as the j loop is done with
-// it, so the epilogue and the next anchors overlap the copy.
-template <int K, int M, int MODE>
-__global__ void __launch_bounds__(GRAD_THREADS) grad_kernel_persistent(const PixArgs a) {
-  __shared__ float s_hh[M == 0 ? MAX_M : 1], s_wh[M == 0 ? MAX_M : 1];
-  extern __shared__ float2 ztile[];
-  stage_consts<M>(a, s_hh, s_wh);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int m = M ? M : (int)a.m;
-  const int S = zstride(m);
-  float2* tile = ztile + (size_t)warp * 32 * S;
-  const long long ntiles = (a.npix + 31) / 32;
-  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  long long tl = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (tl >= ntiles) return;
-  const float2* zg = reinterpret_cast<const float2*>(a.z);
-  float tk[K], ak[K];
-  {
-    const long long i = tl * 32 + lane;
-    load_theta<K>(a, i < a.npix ? i : a.npix - 1, tk, ak);
-    warp_slab_issue(tile, zg + (size_t)tl * 32 * m, (int)min(32ll, a.npix - tl * 32), m, S, lane);
-  }
-  for (; tl < ntiles; tl += nw) {
-    const long long i = tl * 32 + lane;
-    const bool active = i < a.npix;
-    const long long nxt = tl + nw;
-    float tn_[K], an_[K];
-    if (nxt < ntiles) {
-      const long long i2 = nxt * 32 + lane;
-      load_theta<K>(a, i2 < a.npix ? i2 : a.npix - 1, tn_, an_);  // prefetch next theta
-    }
-    float gt[K], ga[K], L;
-    pixel_body<K, M, MODE>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);  // waits for this z slab
-    __syncwarp();  // all lanes are done reading the tile
-    if (nxt < ntiles)
-      warp_slab_issue(tile, zg + (size_t)nxt * 32 * m, (int)min(32ll, a.npix - nxt * 32), m, S, lane);
-    if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-      tk[k] = tn_[k];
-      ak[k] = an_[k];
-    }
-  }
-}
-
 // NEXT-2: `iters` fused data steps per pixel in one launch.
 // The warp stages its z slab once; theta lives in registers across the
 // iterations (each iteration is exactly the PX_GRAD_STEP arithmetic, so the
@@ -484,23 +437,6 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
   const int gwarps = GRAD_THREADS / 32;
   const size_t smem = sizeof(float2) * gwarps * 32 * S;
   const int smem_max = (int)(sizeof(float2) * gwarps * 32 * zstride(MAX_M));
-#if GRAD_PERSISTENT
-  auto fn = grad_kernel_persistent<K, M, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GRAD_THREADS, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const long long ntiles = (a.npix + 31) / 32;
-  long long grid = (ntiles + gwarps - 1) / gwarps;
-  const long long cap = (long long)per_sm * px_num_sms();
-  if (grid > cap) grid = cap;
-#else
   auto fn = grad_kernel<K, M, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -509,7 +445,6 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
     attr_set = true;
   }
   const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
-#endif
   fn<<<(unsigned)grid, GRAD_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
