@@ -438,6 +438,34 @@ def test_iterations_reduce_loss_c1(gpu, oracle_mod, inputs_mod):
     assert err1 < 0.5 * err0
 
 
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_pipeline_host_path_matches_device_path(gpu, inputs_mod, chunks):
+    """FramePipeline.run_host (pinned H2D, pipelined pixel blocks, D2H) returns bitwise the
+    theta of run_device on the same frame (pixels are independent; block boundaries only
+    change launch shapes), for every block count, twice in a row (buffer reuse across steps)."""
+    import torch
+
+    from paper_2203_00952_b200.pipeline import FramePipeline
+
+    f = inputs_mod.make_frame("C2", rows=64, cols=61)
+    t0, a0 = f.theta0()
+    pipe = FramePipeline(f.n_photons, f.npix, f.K, f.T, f.m, f.sigma, iters=7)
+    pipe.load_device(_dev(f.bins), _dev(f.offsets), _dev(t0), _dev(a0))
+    pipe.capture()
+    pipe.run_device()
+    pipe.stream.synchronize()
+    t_ref, a_ref = _host(pipe.t).copy(), _host(pipe.a).copy()
+    pins = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (f.bins, f.offsets, t0, a0)]
+    t_out, a_out = torch.empty_like(pins[2]).pin_memory(), torch.empty_like(pins[3]).pin_memory()
+    for _ in range(2):
+        t_out.zero_()
+        a_out.zero_()
+        pipe.run_host(*pins, t_out, a_out, chunks=chunks)
+        torch.cuda.synchronize()
+        assert np.array_equal(t_out.numpy().view(np.uint32), t_ref.view(np.uint32))
+        assert np.array_equal(a_out.numpy().view(np.uint32), a_ref.view(np.uint32))
+
+
 # ------------------------------------------------ BASELINE configs (C1..C5, C4 sweep)
 def _sample_idx(npix, k, seed):
     rng = np.random.default_rng(seed)
