@@ -46,8 +46,12 @@ def _load():
         lib.srt3d_ref_expected_sketch.argtypes = [P, P, i64, u32, f64, u32, u32, P]
         lib.srt3d_ref_sketch_grad.argtypes = [P, P, P, i64, u32, f64, u32, u32, P, P, P]
         lib.srt3d_ref_descent_update.argtypes = [P, P, P, P, i64, u32, f64, u32, u32, f64]
+        lib.srt3d_ref_backproject.argtypes = [P, i64, f64, u32, u32, u32, P]
+        lib.srt3d_ref_init_depths.argtypes = [P, i64, f64, u32, u32, u32, u32, u32, P, P, P, P]
+        lib.srt3d_ref_init_k1.argtypes = [P, i64, f64, u32, u32, P, P]
         for f in ("srt3d_ref_sketch", "srt3d_ref_phase_index", "srt3d_ref_expected_sketch",
-                  "srt3d_ref_sketch_grad", "srt3d_ref_descent_update"):
+                  "srt3d_ref_sketch_grad", "srt3d_ref_descent_update", "srt3d_ref_backproject",
+                  "srt3d_ref_init_depths", "srt3d_ref_init_k1"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -128,6 +132,46 @@ def descent_update(t, alpha, grad_t, grad_alpha, sigma: float, T: int, m: int, e
                                           float(sigma), T, m, float(eta))
     _check(rc, "srt3d_ref_descent_update")
     return t, alpha
+
+
+def _zd(z):
+    z = np.asarray(z)
+    return np.ascontiguousarray(np.stack([z.real, z.imag], axis=-1), dtype=np.float64)
+
+
+def backproject(z, sigma: float, T: int, N: int) -> np.ndarray:
+    """NEXT-3 (A18): g (npix, N), g[i, n] = Re sum_l z_l hhat_l e^{-i omega_l n T / N}."""
+    zd = _zd(z)
+    npix, m = zd.shape[0], zd.shape[1]
+    g = np.zeros((npix, N), dtype=np.float64)
+    _check(_load().srt3d_ref_backproject(_ptr(zd), npix, float(sigma), T, m, N, _ptr(g)), "srt3d_ref_backproject")
+    return g
+
+
+def init_depths(g, sigma: float, T: int, m: int, K: int, min_sep: int):
+    """NEXT-3 (A19): greedy picks from a backprojection g (npix, N).
+    Returns (t (npix, K), g_at_picks (npix, K), alpha (npix, K), count (npix,))."""
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    npix, N = g.shape
+    t = np.zeros((npix, K))
+    gv = np.zeros((npix, K))
+    a = np.zeros((npix, K))
+    c = np.zeros(npix, dtype=np.int32)
+    rc = _load().srt3d_ref_init_depths(_ptr(g), npix, float(sigma), T, m, N, K, int(min_sep), _ptr(t), _ptr(gv),
+                                       _ptr(a), _ptr(c))
+    _check(rc, "srt3d_ref_init_depths")
+    return t, gv, a, c
+
+
+def init_k1(z, sigma: float, T: int):
+    """NEXT-3 (A20): K = 1 closed-form depth from arg(z_1) and least-squares alpha.
+    Returns (t (npix,), alpha (npix,))."""
+    zd = _zd(z)
+    npix, m = zd.shape[0], zd.shape[1]
+    t = np.zeros(npix)
+    a = np.zeros(npix)
+    _check(_load().srt3d_ref_init_k1(_ptr(zd), npix, float(sigma), T, m, _ptr(t), _ptr(a)), "srt3d_ref_init_k1")
+    return t, a
 
 
 def set_threads(n: int) -> None:

@@ -22,6 +22,15 @@
  *   srt3d_ref_phase_index      the integer phase index r = (j*x) mod T that
  *                              omega_j * x_p reduces to (P:61 + P:84).
  *   srt3d_ref_descent_update   the harness update rule (reading A13).
+ *   srt3d_ref_backproject      NEXT-3 matched-filter backprojection
+ *                              g(t) = Re sum_l z_l conj(hhat_l) e^{-i omega_l t}
+ *                              on the grid t_i = i T / N (A18).
+ *   srt3d_ref_init_depths      NEXT-3 greedy pick of up to K local maxima of
+ *                              g with a minimum circular separation (
+ *                              A19).
+ *   srt3d_ref_init_k1          NEXT-3 K = 1 closed form: depth from the phase
+ *                              of z_1, intensity by K = 1 least squares
+ *                              (A20).
  *
  * Everything is computed in double precision with the textbook formula, in
  * the order the definition states; OpenMP only splits independent pixels.
@@ -217,6 +226,133 @@ int srt3d_ref_descent_update(double* t, double* alpha, const double* grad_t, con
     if (an < 0.0) an = 0.0;
     if (an > 1.0) an = 1.0;
     alpha[q] = an;
+  }
+  return REF_OK;
+}
+
+/* ---- NEXT-3: pixelwise initialisation (A18-A20) ---- */
+
+/* g[i][n] = Re sum_{l=1..m} z_l * hhat_l * exp(-i * omega_l * t_n), t_n = n*T/N,
+ * omega_l = 2*pi*l/T, hhat real (Gaussian, reading A5) so conj(hhat) = hhat.
+ * The phase omega_l * t_n = 2*pi*l*n/N is reduced exactly as (l*n) mod N. */
+int srt3d_ref_backproject(const double* z, int64_t npix, double sigma, uint32_t T, uint32_t m,
+                          uint32_t N, double* g) {
+  if (T < 1 || m < 1 || N < 1 || npix < 0 || !(sigma >= 0.0)) return REF_EINVAL;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < npix; i++) {
+    for (uint32_t n = 0; n < N; n++) {
+      double acc = 0.0;
+      for (uint32_t l = 1; l <= m; l++) {
+        double omega = 2.0 * M_PI * (double)l / (double)T;
+        double hhat = exp(-sigma * sigma * omega * omega / 2.0);
+        uint64_t r = ((uint64_t)l * (uint64_t)n) % (uint64_t)N;
+        double ph = -2.0 * M_PI * (double)r / (double)N;
+        double zre = z[((size_t)i * m + (l - 1)) * 2], zim = z[((size_t)i * m + (l - 1)) * 2 + 1];
+        /* Re((zre + i zim) * hhat * (cos ph + i sin ph)) */
+        acc += hhat * (zre * cos(ph) - zim * sin(ph));
+      }
+      g[(size_t)i * N + n] = acc;
+    }
+  }
+  return REF_OK;
+}
+
+/* Greedy initial depths from g (one pixel row of N values, grid t_n = n*T/N):
+ *   candidates: n with g_n > 0, g_n > g_{n-1} and g_n >= g_{n+1} (circular, N >= 3);
+ *   K times: the candidate with the largest g (ties: smallest n) whose circular
+ *   grid distance d to every earlier pick satisfies d*T >= min_sep*N.
+ * Outputs, sorted by depth: t_out[k] = n_k*T/N, g_out[k] = g_{n_k}, and
+ * alpha_out[k] = clamp(g_{n_k} / sum_l hhat_l^2, 0, 1); count[i] = picks.
+ * Unfilled slots (reading A14): t = (t_first + T/2) mod T (T/2 if none),
+ * g = alpha = 0.  Input g is the fp64 backprojection above. */
+int srt3d_ref_init_depths(const double* g, int64_t npix, double sigma, uint32_t T, uint32_t m, uint32_t N,
+                          uint32_t K, uint32_t min_sep, double* t_out, double* g_out, double* alpha_out,
+                          int32_t* count) {
+  if (T < 1 || m < 1 || N < 3 || K < 1 || npix < 0 || !(sigma >= 0.0)) return REF_EINVAL;
+  double sh2 = 0.0;
+  for (uint32_t l = 1; l <= m; l++) {
+    double omega = 2.0 * M_PI * (double)l / (double)T;
+    double hhat = exp(-sigma * sigma * omega * omega / 2.0);
+    sh2 += hhat * hhat;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < npix; i++) {
+    const double* gi = g + (size_t)i * N;
+    uint32_t pick[64];
+    uint32_t c = 0;
+    for (uint32_t k = 0; k < K && k < 64; k++) {
+      int64_t best = -1;
+      for (uint32_t n = 0; n < N; n++) {
+        double gp = gi[(n + N - 1) % N], gn = gi[(n + 1) % N];
+        if (!(gi[n] > 0.0 && gi[n] > gp && gi[n] >= gn)) continue;
+        int ok = 1;
+        for (uint32_t q = 0; q < c; q++) {
+          uint32_t d = n > pick[q] ? n - pick[q] : pick[q] - n;
+          if (N - d < d) d = N - d;
+          if ((uint64_t)d * T < (uint64_t)min_sep * N) ok = 0;
+        }
+        if (ok && (best < 0 || gi[n] > gi[best])) best = n;
+      }
+      if (best < 0) break;
+      pick[c++] = (uint32_t)best;
+    }
+    /* sort picks by grid index (= depth) */
+    for (uint32_t a = 1; a < c; a++)
+      for (uint32_t b = a; b > 0 && pick[b - 1] > pick[b]; b--) {
+        uint32_t tmp = pick[b];
+        pick[b] = pick[b - 1];
+        pick[b - 1] = tmp;
+      }
+    double tfirst = c ? (double)pick[0] * (double)T / (double)N : 0.0;
+    for (uint32_t k = 0; k < K; k++) {
+      size_t o = (size_t)i * K + k;
+      if (k < c) {
+        double gv = gi[pick[k]];
+        double a = gv / sh2;
+        t_out[o] = (double)pick[k] * (double)T / (double)N;
+        g_out[o] = gv;
+        alpha_out[o] = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);
+      } else {
+        t_out[o] = fmod(tfirst + 0.5 * (double)T, (double)T);
+        g_out[o] = 0.0;
+        alpha_out[o] = 0.0;
+      }
+    }
+    count[i] = (int32_t)c;
+  }
+  return REF_OK;
+}
+
+/* K = 1 closed form: t = (T / 2 pi) * arg(z_1 * conj(hhat_1)) mapped into
+ * [0, T) (hhat_1 > 0, so arg(z_1)); alpha = clamp(sum_l hhat_l Re(conj(e^{i omega_l t}) z_l)
+ * / sum_l hhat_l^2, 0, 1), the least-squares alpha at t.  |z_1| <= 1e-12:
+ * t = alpha = 0. */
+int srt3d_ref_init_k1(const double* z, int64_t npix, double sigma, uint32_t T, uint32_t m, double* t_out,
+                      double* alpha_out) {
+  if (T < 1 || m < 1 || npix < 0 || !(sigma >= 0.0)) return REF_EINVAL;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < npix; i++) {
+    double z1re = z[(size_t)i * m * 2], z1im = z[(size_t)i * m * 2 + 1];
+    if (hypot(z1re, z1im) <= 1e-12) {
+      t_out[i] = 0.0;
+      alpha_out[i] = 0.0;
+      continue;
+    }
+    double t = (double)T * atan2(z1im, z1re) / (2.0 * M_PI);
+    if (t < 0.0) t += (double)T;
+    if (t >= (double)T) t -= (double)T;
+    double num = 0.0, den = 0.0;
+    for (uint32_t l = 1; l <= m; l++) {
+      double omega = 2.0 * M_PI * (double)l / (double)T;
+      double hhat = exp(-sigma * sigma * omega * omega / 2.0);
+      double zre = z[((size_t)i * m + (l - 1)) * 2], zim = z[((size_t)i * m + (l - 1)) * 2 + 1];
+      /* Re(conj(cos + i sin) * z) = cos * zre + sin * zim */
+      num += hhat * (cos(omega * t) * zre + sin(omega * t) * zim);
+      den += hhat * hhat;
+    }
+    double a = num / den;
+    t_out[i] = t;
+    alpha_out[i] = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);
   }
   return REF_OK;
 }

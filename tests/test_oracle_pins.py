@@ -317,3 +317,95 @@ def test_update_is_diagonal_gauss_newton(oracle_mod):
     tn, an = oracle_mod.descent_update(np.array([[1.0]]), np.array([[0.5]]), np.array([[1e9]]), np.array([[1e9]]),
                                        sigma, T, m, eta=0.5)
     assert abs(tn[0, 0] - (1.0 - T / (4 * m) + T)) < 1e-9 and an[0, 0] == 0.0
+
+
+# ------------------------------------------- NEXT-3 initialisation (A18-A20)
+def _dirichlet(phi, m):
+    """sum_{l=1..m} cos(l phi) in closed form (phi = 0 -> m)."""
+    phi = np.asarray(phi, dtype=np.float64)
+    out = np.full(phi.shape, float(m))
+    nz = np.abs(np.sin(phi / 2)) > 1e-12
+    out[nz] = np.sin(m * phi[nz] / 2) * np.cos((m + 1) * phi[nz] / 2) / np.sin(phi[nz] / 2)
+    return out
+
+
+@pytest.mark.parametrize("T,m,N", [(1024, 4, 1024), (4613, 10, 4613), (8192, 32, 256), (100, 7, 25)])
+def test_BP1_single_photon_dirichlet(oracle_mod, T, m, N):
+    """BP1: one photon at x, delta IRF -> g(t) is the Dirichlet kernel
+    sum_l cos(omega_l (x - t)) in closed form; its maximum m sits at t = x."""
+    x = (37 * T) // 100
+    z = oracle_mod.sketch(np.array([x], np.uint16), np.array([0, 1], np.uint32), T, m)
+    g = oracle_mod.backproject(z, 0.0, T, N)[0]
+    tn = np.arange(N) * T / N
+    np.testing.assert_allclose(g, _dirichlet(2 * np.pi * (x - tn) / T, m), atol=1e-11)
+    if (x * N) % T == 0:
+        assert np.argmax(g) == x * N // T and abs(g.max() - m) < 1e-12
+
+
+def test_BP2_coefficients_recovered_by_grid_dft(oracle_mod):
+    """BP2: for N > 2m the grid values determine the coefficients: (2/N) sum_n g_n e^{+i omega_l t_n}
+    = hhat_l z_l (discrete orthogonality) — fixes the sign of the exponent and the hhat weight."""
+    rng = np.random.default_rng(3)
+    T, m, N, sigma = 2500, 20, 64, 3.0
+    z = (rng.normal(size=m) + 1j * rng.normal(size=m))[None, :]
+    g = oracle_mod.backproject(z, sigma, T, N)[0]
+    w, h = _hhat(sigma, T, m)
+    tn = np.arange(N) * T / N
+    rec = np.array([(2.0 / N) * np.sum(g * np.exp(1j * wl * tn)) for wl in w])
+    np.testing.assert_allclose(rec, h * z[0], atol=1e-12)
+
+
+def test_BP3_bound_and_shift(oracle_mod, inputs_mod):
+    """BP3: |g| <= sum_l hhat_l |z_l| (triangle inequality); shifting every photon by
+    s = k T/N bins shifts g by k grid points."""
+    T, m, N, sigma = 4096, 10, 512, 4.0
+    bins, offs = inputs_mod.random_csr(npix=20, T=T, max_n=400, seed=5)
+    z = oracle_mod.sketch(bins, offs, T, m)
+    g = oracle_mod.backproject(z, sigma, T, N)
+    _, h = _hhat(sigma, T, m)
+    assert np.all(np.abs(g) <= np.sum(h * np.abs(z), axis=1)[:, None] + 1e-12)
+    k = 13
+    zs = oracle_mod.sketch(((bins.astype(np.int64) + k * T // N) % T).astype(np.uint16), offs, T, m)
+    np.testing.assert_allclose(oracle_mod.backproject(zs, sigma, T, N), np.roll(g, k, axis=1), atol=1e-9)
+
+
+def test_ID_greedy_picks(oracle_mod):
+    """ID: single photon -> its bin; two photons farther apart than min_sep -> both,
+    sorted; closer than min_sep -> one peak (a further pick is a weak side lobe); flat zero
+    sketch -> none, unfilled slots per A14."""
+    T, m, N = 1024, 16, 1024
+    def picks(xs, K, min_sep, weights=None):
+        lists = np.array(xs, np.uint16)
+        z = oracle_mod.sketch(lists, np.array([0, len(xs)], np.uint32), T, m)
+        g = oracle_mod.backproject(z, 0.0, T, N)
+        return oracle_mod.init_depths(g, 0.0, T, m, K, min_sep)
+    t, gv, a, c = picks([300], 1, 10)
+    assert c[0] == 1 and t[0, 0] == 300.0 and abs(gv[0, 0] - m) < 1e-12 and a[0, 0] == 1.0
+    t, gv, a, c = picks([700, 200], 2, 50)
+    assert c[0] == 2 and abs(t[0, 0] - 200) <= 1 and abs(t[0, 1] - 700) <= 1  # within one grid step (S:310)
+    t, gv, a, c = picks([500, 520], 2, 50)  # one merged peak; the second pick is a side lobe (S:317)
+    main = int(np.argmax(gv[0]))
+    assert 490 <= t[0, main] <= 530 and c[0] == 2
+    assert gv[0, 1 - main] < 0.3 * gv[0, main] and abs(t[0, 1] - t[0, 0]) >= 50
+    t, gv, a, c = picks([500, 520], 1, 50)
+    assert c[0] == 1 and 490 <= t[0, 0] <= 530
+    g0 = np.zeros((1, N))
+    t, gv, a, c = oracle_mod.init_depths(g0, 0.0, T, m, 3, 10)
+    assert c[0] == 0 and np.all(a == 0) and np.all(t == T / 2)
+
+
+def test_IK_closed_form_k1(oracle_mod):
+    """IK: single photon at v -> v; noiseless K=1 sketch at t = 1000, T = 4613,
+    sigma = 10 -> 1000 within 1e-9 and alpha recovered (S:108 least squares); z = 0 -> 0."""
+    T = 4613
+    z = oracle_mod.sketch(np.array([1234], np.uint16), np.array([0, 1], np.uint32), T, 5)
+    t, a = oracle_mod.init_k1(z, 0.0, T)
+    assert abs(t[0] - 1234) < 1e-9 and abs(a[0] - 1) < 1e-12
+    z = oracle_mod.expected_sketch(np.array([[1000.0]]), np.array([[0.37]]), 10.0, T, 10)
+    t, a = oracle_mod.init_k1(z, 10.0, T)
+    assert abs(t[0] - 1000.0) < 1e-9 and abs(a[0] - 0.37) < 1e-12
+    z = oracle_mod.expected_sketch(np.array([[4612.75]]), np.array([[0.5]]), 3.0, T, 4)
+    t, a = oracle_mod.init_k1(z, 3.0, T)
+    assert abs(t[0] - 4612.75) < 1e-9 and 0 <= t[0] < T
+    t, a = oracle_mod.init_k1(np.zeros((2, 4), complex), 1.0, T)
+    assert np.all(t == 0) and np.all(a == 0)
