@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pixel blocks pipelined H2D/compute in the e2e path")
+    ap.add_argument("--no-init", action="store_true", help="skip the NEXT-3 initialisation timings")
+    ap.add_argument("--init-grid", type=int, default=0, help="backprojection grid points (default 16 m)")
+    ap.add_argument("--init-min-sep", type=int, default=50, help="minimum separation of initial depths (bins)")
     return ap.parse_args()
 
 
@@ -322,6 +325,28 @@ def run_srt3d(args):
         grad_cold_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in times[1:])
         del flush
 
+    # NEXT-3 initialisation kernels on this frame's sketch (outside the timed
+    # step, which starts from theta0 = t* + 10 per BASELINE.json): greedy
+    # backprojection depths (grid N, K picks) and the K = 1 closed form.
+    init_ms = None
+    if not args.no_init:
+        N_grid = min(4096, max(3, args.init_grid or 16 * f.m))
+        min_sep = args.init_min_sep
+        with torch.cuda.stream(s):
+            srt3d.srt3d_init_depths(pipe.z, f.sigma, f.T, N_grid, f.K, min_sep)
+            srt3d.srt3d_init_k1(pipe.z, f.sigma, f.T)
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(5)]
+            for e in ev:
+                e[0].record(s)
+                srt3d.srt3d_init_depths(pipe.z, f.sigma, f.T, N_grid, f.K, min_sep)
+                e[1].record(s)
+                srt3d.srt3d_init_k1(pipe.z, f.sigma, f.T)
+                e[2].record(s)
+        s.synchronize()
+        init_ms = {"N": N_grid, "K": f.K, "min_sep": min_sep,
+                   "depths_ms": statistics.median(e[0].elapsed_time(e[1]) for e in ev),
+                   "k1_ms": statistics.median(e[1].elapsed_time(e[2]) for e in ev)}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -374,6 +399,23 @@ def run_srt3d(args):
                         "across iterations, so algorithmic bytes / time can exceed the HBM copy peak",
                 "cold_l2_ms_per_launch": grad_cold_ms,
                 "cold_l2_roofline": roofline(kname, g_bytes, g_flops, grad_cold_ms) if grad_cold_ms else None}
+    init = None
+    if init_ms is not None:
+        # backprojection + picks: F = 8 m N per pixel (one complex multiply-add per (grid point, l));
+        # B = 8 m + 12 K + 4 per pixel.  K = 1 closed form: B = 8 m + 8, F = 8 m per pixel (phasor
+        # step + weighted real part), HBM-bound.
+        d_b = f.npix * (8.0 * f.m + 12.0 * f.K + 4.0)
+        d_f = f.npix * 8.0 * f.m * init_ms["N"]
+        k_b = f.npix * (8.0 * f.m + 8.0)
+        k_f = f.npix * 8.0 * f.m
+        init = {"init_depths": {"kernel": "srt3d_init_depths", "grid_N": init_ms["N"], "K": init_ms["K"],
+                                "min_sep": init_ms["min_sep"], "ms": init_ms["depths_ms"],
+                                "pixels_per_s": f.npix / (init_ms["depths_ms"] * 1e-3),
+                                "roofline": roofline("srt3d_init_depths", d_b, d_f, init_ms["depths_ms"])},
+                "init_k1": {"kernel": "srt3d_init_k1", "ms": init_ms["k1_ms"],
+                            "pixels_per_s": f.npix / (init_ms["k1_ms"] * 1e-3),
+                            "roofline": roofline("srt3d_init_k1", k_b, k_f, init_ms["k1_ms"])},
+                "note": "NEXT-3, timed outside the step (the step starts from theta0 = t* + 10)"}
     # dominant kernel (larger share of the step) -> the line's roofline object
     traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -401,7 +443,7 @@ def run_srt3d(args):
             "data": "synthetic (seeded Eq. (1) photon frames; stand-in for the paper's head/camouflage datasets)",
             "config": config_obj(f, args), "clocks": clocks, "e2e": e2e,
             "gpu_launches": pipe.launches_per_step * args.steps,
-            "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad,
+            "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad, "init": init,
             "step_definition": "srt3d_sketch over the frame + iters x srt3d_sketch_grad_step (CUDA graphs)"}
     print(json.dumps(line), flush=True)
     if world > 1:

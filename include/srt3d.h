@@ -183,6 +183,42 @@ int srt3d_fit_pixelwise(const float* z, float* t, float* alpha, int64_t npix, ui
                         uint32_t m, float eta, uint32_t iters, float* loss, void* stream);
 
 /*
+ * NEXT-3 — pixelwise initialisation of the sketched fit.  The
+ * paper gives no initializer for Eq. (6); these follow the
+ * matched-filter / phase readings A18-A20 of DESIGN.md.
+ *
+ * srt3d_backproject — g[i][n] = Re sum_{l=1..m} z_l hhat(omega_l) e^{-i omega_l t_n},
+ * t_n = n*T/N, n = 0..N-1 (a circular grid), hhat Gaussian with sigma.
+ *   z  float [npix][m][2] (8-byte aligned); g float [npix][N] output.
+ *   1 <= N <= 8192.  Errors as srt3d_expected_sketch; N out of range: EINVAL.
+ */
+int srt3d_backproject(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, uint32_t N, float* g,
+                      void* stream);
+
+/*
+ * srt3d_init_depths — up to K initial depths per pixel from g (reading A19):
+ * candidates are grid points with g_n > 0, g_n > g_{n-1}, g_n >= g_{n+1}
+ * (circular); K times the largest (ties: smallest n) whose circular distance
+ * d (grid steps) to every earlier pick has d*T >= min_sep*N.  Outputs, sorted
+ * by depth: t [npix][K] = n*T/N, g_at [npix][K], alpha [npix][K] =
+ * clamp(g_at / sum_l hhat_l^2, 0, 1), count [npix] (int32) = picks made.
+ * Unfilled slots (reading A14): t = (t_first + T/2) mod T, g_at = alpha = 0.
+ *   3 <= N <= 4096, 1 <= K <= SRT3D_MAX_K, min_sep in bins.
+ */
+int srt3d_init_depths(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, uint32_t N, uint32_t K,
+                      uint32_t min_sep, float* t, float* g_at, float* alpha, int32_t* count, void* stream);
+
+/*
+ * srt3d_init_k1 — K = 1 closed form (reading A20):
+ * t[i] = (T / 2 pi) arg(z_1) mapped into [0, T) (hhat_1 > 0 leaves the phase
+ * unchanged); alpha[i] = clamp(sum_l hhat_l Re(conj(e^{i omega_l t}) z_l) /
+ * sum_l hhat_l^2, 0, 1), the least-squares intensity at t.
+ * |z_1| <= 1e-12: t = alpha = 0.   t, alpha float [npix] outputs.
+ */
+int srt3d_init_k1(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, float* t, float* alpha,
+                  void* stream);
+
+/*
  * srt3d_check_csr — debug validator (not on the hot path).  Sets *bad (a
  * device int32 the caller zeroes first) to non-zero if some bins[p] >= T or
  * some offsets[i+1] < offsets[i].

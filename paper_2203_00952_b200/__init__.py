@@ -36,7 +36,8 @@ PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT, PATH_PAIRED = 0, 1, 2, 3
 EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
            "srt3d_sketch_grad",
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
-           "srt3d_sketch_plan", "srt3d_fit_pixelwise")
+           "srt3d_sketch_plan", "srt3d_fit_pixelwise",
+           "srt3d_backproject", "srt3d_init_depths", "srt3d_init_k1")
 
 
 class Srt3dError(RuntimeError):
@@ -70,6 +71,9 @@ def load_library(path: str | None = None):
     lib.srt3d_debug_phase_index.argtypes = [P, i64, u32, u32, P, P]
     lib.srt3d_sketch_plan.argtypes = [i64, u32, u32, u64, P]
     lib.srt3d_fit_pixelwise.argtypes = [P, P, P, i64, u32, f32, u32, u32, f32, u32, P, P]
+    lib.srt3d_backproject.argtypes = [P, i64, f32, u32, u32, u32, P, P]
+    lib.srt3d_init_depths.argtypes = [P, i64, f32, u32, u32, u32, u32, u32, P, P, P, P, P]
+    lib.srt3d_init_k1.argtypes = [P, i64, f32, u32, u32, P, P, P]
     for f in EXPORTS[2:]:
         getattr(lib, f).restype = ctypes.c_int
     if path is None:
@@ -180,6 +184,41 @@ def srt3d_fit_pixelwise(z, t, alpha, sigma: float, T: int, m: int, iters: int, e
     _call("srt3d_fit_pixelwise", _ptr(z), _ptr(t), _ptr(alpha), npix, K, float(sigma), T, m, float(eta), int(iters),
           _ptr(loss), _stream(stream))
     return t, alpha
+
+
+def srt3d_backproject(z, sigma: float, T: int, N: int, g=None, stream=None):
+    """NEXT-3: matched-filter backprojection on the circular grid t_n = n T / N: float32 (npix, N)."""
+    npix, m = z.shape
+    if g is None:
+        g = torch.empty((npix, N), dtype=torch.float32, device=z.device)
+    _need_cuda(z, g)
+    _call("srt3d_backproject", _ptr(z), npix, float(sigma), T, m, N, _ptr(g), _stream(stream))
+    return g
+
+
+def srt3d_init_depths(z, sigma: float, T: int, N: int, K: int, min_sep: int, stream=None):
+    """NEXT-3: up to K greedy backprojection peaks per pixel -> (t, g_at, alpha) float32 (npix, K),
+    count int32 (npix,)."""
+    npix, m = z.shape
+    dev = z.device
+    t = torch.empty((npix, K), dtype=torch.float32, device=dev)
+    g = torch.empty_like(t)
+    a = torch.empty_like(t)
+    c = torch.empty(npix, dtype=torch.int32, device=dev)
+    _need_cuda(z)
+    _call("srt3d_init_depths", _ptr(z), npix, float(sigma), T, m, N, K, int(min_sep), _ptr(t), _ptr(g), _ptr(a),
+          _ptr(c), _stream(stream))
+    return t, g, a, c
+
+
+def srt3d_init_k1(z, sigma: float, T: int, stream=None):
+    """NEXT-3: K = 1 closed-form depth (phase of z_1) and least-squares alpha: float32 (npix, 1) each."""
+    npix, m = z.shape
+    t = torch.empty((npix, 1), dtype=torch.float32, device=z.device)
+    a = torch.empty_like(t)
+    _need_cuda(z)
+    _call("srt3d_init_k1", _ptr(z), npix, float(sigma), T, m, _ptr(t), _ptr(a), _stream(stream))
+    return t, a
 
 
 def srt3d_check_csr(bins, offsets, T: int, stream=None) -> int:

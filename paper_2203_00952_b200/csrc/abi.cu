@@ -291,6 +291,84 @@ int srt3d_fit_pixelwise(const float* z, float* t, float* alpha, int64_t npix, ui
   return SRT3D_OK;
 }
 
+// ---- NEXT-3 initialisation ---------------------------------------------------
+static int init_args(srt3d::BpArgs& b, const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m) {
+  int rc = check_kparams(npix, 1, sigma, T, m);
+  if (rc) return rc;
+  srt3d::PixArgs pa = {};
+  fill_consts(pa, sigma, T, m, 1.f);
+  double sh2 = 0.0;
+  for (uint32_t j = 1; j <= m; j++) {
+    const double w = 2.0 * 3.14159265358979323846 * (double)j / (double)T;
+    const double h = std::exp(-(double)sigma * (double)sigma * w * w / 2.0);
+    sh2 += h * h;
+  }
+  b = {};
+  for (int j = 0; j < srt3d::MAX_M; j++) b.hh[j] = pa.c.hh[j];
+  b.inv_sh2 = (float)(1.0 / sh2);
+  b.z = z;
+  b.npix = npix;
+  b.T = T;
+  b.m = m;
+  return SRT3D_OK;
+}
+
+int srt3d_backproject(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, uint32_t N, float* g,
+                      void* stream) {
+  srt3d::BpArgs b;
+  int rc = init_args(b, z, npix, sigma, T, m);
+  if (rc) return rc;
+  if (N < 1 || N > 8192) return fail(SRT3D_EINVAL, "N=%u must be in [1, 8192]", N);
+  if (npix == 0) return SRT3D_OK;
+  if (!z || !g) return fail(SRT3D_ENULL, "z/g must be non-NULL");
+  if (!aligned(z, 8) || !aligned(g, 4)) return fail(SRT3D_EALIGN, "z must be 8-byte and g 4-byte aligned");
+  b.g = g;
+  b.N = N;
+  cudaError_t e = srt3d::launch_backproject(b, false, (cudaStream_t)stream, num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_backproject");
+  return SRT3D_OK;
+}
+
+int srt3d_init_depths(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, uint32_t N, uint32_t K,
+                      uint32_t min_sep, float* t, float* g_at, float* alpha, int32_t* count, void* stream) {
+  srt3d::BpArgs b;
+  int rc = init_args(b, z, npix, sigma, T, m);
+  if (rc) return rc;
+  if (N < 3 || N > 4096) return fail(SRT3D_EINVAL, "N=%u must be in [3, 4096]", N);
+  if (K < 1) return fail(SRT3D_EINVAL, "K=%u < 1", K);
+  if (K > SRT3D_MAX_K) return fail(SRT3D_EUNSUPPORTED, "K=%u exceeds SRT3D_MAX_K=%u", K, SRT3D_MAX_K);
+  if (npix == 0) return SRT3D_OK;
+  if (!z || !t || !g_at || !alpha || !count) return fail(SRT3D_ENULL, "z/t/g_at/alpha/count must be non-NULL");
+  if (!aligned(z, 8) || !aligned(t, 4) || !aligned(g_at, 4) || !aligned(alpha, 4) || !aligned(count, 4))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and the outputs 4-byte aligned");
+  b.N = N;
+  b.K = K;
+  b.min_sep = min_sep;
+  b.t_out = t;
+  b.g_out = g_at;
+  b.a_out = alpha;
+  b.count = count;
+  cudaError_t e = srt3d::launch_backproject(b, true, (cudaStream_t)stream, num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_init_depths");
+  return SRT3D_OK;
+}
+
+int srt3d_init_k1(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, float* t, float* alpha,
+                  void* stream) {
+  srt3d::BpArgs b;
+  int rc = init_args(b, z, npix, sigma, T, m);
+  if (rc) return rc;
+  if (npix == 0) return SRT3D_OK;
+  if (!z || !t || !alpha) return fail(SRT3D_ENULL, "z/t/alpha must be non-NULL");
+  if (!aligned(z, 8) || !aligned(t, 4) || !aligned(alpha, 4))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and t/alpha 4-byte aligned");
+  b.t_out = t;
+  b.a_out = alpha;
+  cudaError_t e = srt3d::launch_init_k1(b, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_init_k1");
+  return SRT3D_OK;
+}
+
 int srt3d_check_csr(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, int32_t* bad,
                     void* stream) {
   if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);

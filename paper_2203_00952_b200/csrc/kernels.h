@@ -72,6 +72,22 @@ cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, ui
 cudaError_t launch_check_csr(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,
                              int32_t* bad, cudaStream_t s, int num_sms);
 cudaError_t launch_pixel(PixMode mode, int K, const PixArgs& a, cudaStream_t s);
+// NEXT-3 initialisation kernels (init.cu).
+struct BpArgs {
+  const float* z;   // [npix][m][2]
+  float* g;         // backprojection output [npix][N] (or null)
+  float* t_out;     // picks [npix][K] (init_depths) or [npix] (init_k1)
+  float* g_out;
+  float* a_out;
+  int32_t* count;
+  long long npix;
+  uint32_t T, m, N, K, min_sep;
+  float inv_sh2;    // 1 / sum_l hhat_l^2
+  float hh[MAX_M];  // hhat_l
+};
+cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int num_sms);
+cudaError_t launch_init_k1(const BpArgs& a, cudaStream_t s);
+size_t backproject_smem(uint32_t N, bool pick);
 cudaError_t launch_fit(int K, const PixArgs& a, int iters, cudaStream_t s);
 
 }  // namespace srt3d

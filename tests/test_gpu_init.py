@@ -1,0 +1,168 @@
+"""NEXT-3 GPU <-> oracle parity: backprojection, greedy initial
+depths and the K = 1 closed form, through the C ABI, on the same fp32 sketches.
+
+Tolerances (readings A18-A20):
+  * g: |delta| <= 1e-5 * S_i, S_i = sum_l hhat_l |z_il| (the triangle bound of g);
+    Horner in fp32 over m <= 64 terms errs by <= 2 m eps S_i = 7.6e-6 S_i.
+  * picks (integers decided by fp comparisons): identical where the oracle's
+    decision is not a near-tie (margin > 2e-5 S_i); otherwise the GPU pick must be
+    a valid choice within that margin.
+  * init_k1: t within 0.5 fp32 ulp of T (both sides take fp64 atan2 of the same
+    z_1; the GPU rounds t to fp32), circularly; alpha within 1e-4 * S_alpha,
+    S_alpha = sum_l hhat_l |z_l| / sum_l hhat_l^2.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _hh(sigma, T, m):
+    w = 2 * np.pi * np.arange(1, m + 1) / T
+    return np.exp(-(sigma**2) * w**2 / 2)
+
+
+def _gpu_sketch(gpu, bins, offs, T, m):
+    import torch
+
+    z = gpu.srt3d_sketch(_dev(bins), _dev(offs), T, m, total_photons=int(offs[-1]))
+    torch.cuda.synchronize()
+    return z
+
+
+@pytest.mark.parametrize("T,m,N,sigma", [(1024, 4, 1024, 2.0), (4613, 10, 300, 5.0), (2500, 20, 129, 3.0),
+                                         (8192, 32, 8192, 6.0), (8192, 64, 1000, 0.0), (100, 1, 7, 0.0),
+                                         (17, 16, 1, 1.0), (4096, 10, 4096, 4.0)])
+def test_backproject_parity(gpu, oracle_mod, inputs_mod, T, m, N, sigma):
+    import torch
+
+    bins, offs = inputs_mod.random_csr(npix=203, T=T, max_n=600, seed=T + m + N)
+    z = _gpu_sketch(gpu, bins, offs, T, m)
+    g = gpu.srt3d_backproject(z, sigma, T, N)
+    torch.cuda.synchronize()
+    zh = z.cpu().numpy()
+    go = oracle_mod.backproject(zh, sigma, T, N)
+    S = np.sum(_hh(sigma, T, m) * np.abs(zh), axis=1)[:, None]
+    d = np.abs(g.cpu().numpy() - go)
+    assert np.all(d <= 1e-5 * S + 1e-30), float((d / (S + 1e-30)).max())
+
+
+def _check_picks(tg, cg, tol_g, to, co, go_row_fn, T, N, min_sep):
+    """Exact match unless the oracle faced a near-tie; then the GPU's pick must be valid."""
+    bad = 0
+    for i in range(tg.shape[0]):
+        if cg[i] == co[i] and np.array_equal(tg[i], to[i]):
+            continue
+        g = go_row_fn(i)
+        n_g = np.rint(tg[i, : cg[i]] * N / T).astype(np.int64) % N
+        cand = (g > -tol_g[i]) & (g >= np.roll(g, 1) - tol_g[i]) & (g >= np.roll(g, -1) - tol_g[i])
+        assert np.all(cand[n_g]), i
+        for a in range(len(n_g)):
+            for b in range(a + 1, len(n_g)):
+                d = abs(n_g[a] - n_g[b])
+                assert min(d, N - d) * T >= min_sep * N, i
+        # a near-tie: the best oracle value among GPU picks and oracle picks agree within tol
+        gg = np.sort(g[n_g])[::-1]
+        n_o = np.rint(to[i, : co[i]] * N / T).astype(np.int64) % N
+        oo = np.sort(g[n_o])[::-1]
+        k = min(len(gg), len(oo))
+        assert np.all(np.abs(gg[:k] - oo[:k]) <= 4 * tol_g[i]) or abs(int(cg[i]) - int(co[i])) <= 1, i
+        bad += 1
+    return bad
+
+
+@pytest.mark.parametrize("T,m,N,K,min_sep,sigma", [(8192, 32, 512, 3, 50, 6.0), (2500, 20, 256, 2, 40, 3.0),
+                                                   (1024, 4, 64, 1, 10, 2.0), (4613, 10, 4096, 8, 30, 5.0),
+                                                   (100, 7, 3, 2, 1, 0.0)])
+def test_init_depths_parity(gpu, oracle_mod, inputs_mod, T, m, N, K, min_sep, sigma):
+    """Greedy picks on (a) noiseless multi-surface sketches (well separated: exact match required
+    for every pixel) and (b) sketches of noisy ragged frames (near-ties allowed, see module doc)."""
+    import torch
+
+    rng = np.random.default_rng(T + K)
+    npix = 150
+    # (a) noiseless: K surfaces >= 4 * min_sep apart, alpha in [0.2, 1]
+    Kt = min(K, 3)
+    base = rng.uniform(0, T, npix)
+    t = np.stack([(base + k * max(4 * min_sep, T // (Kt + 1))) % T for k in range(Kt)], axis=1).astype(np.float32)
+    a = rng.uniform(0.2, 1.0, (npix, Kt)).astype(np.float32)
+    z_a = gpu.srt3d_expected_sketch(_dev(t), _dev(a), sigma, T, m)
+    # (b) noisy ragged frame
+    bins, offs = inputs_mod.random_csr(npix=npix, T=T, max_n=400, seed=T + m)
+    z_b = _gpu_sketch(gpu, bins, offs, T, m)
+    for z, exact in ((z_a, True), (z_b, False)):
+        tg, gg, ag, cg = gpu.srt3d_init_depths(z, sigma, T, N, K, min_sep)
+        torch.cuda.synchronize()
+        zh = z.cpu().numpy()
+        gfull = oracle_mod.backproject(zh, sigma, T, N)
+        to, go, ao, co = oracle_mod.init_depths(gfull, sigma, T, m, K, min_sep)
+        tg, gg, ag, cg = (x.cpu().numpy() for x in (tg, gg, ag, cg))
+        S = np.sum(_hh(sigma, T, m) * np.abs(zh), axis=1)
+        tol = 2e-5 * S
+        if exact and N >= 2 * m:
+            match = (cg == co) & np.all(tg == to.astype(np.float32), axis=1)
+            assert match.mean() >= 0.99, match.mean()
+        bad = _check_picks(tg, cg, tol, to.astype(np.float32), co, lambda i: gfull[i], T, N, min_sep)
+        assert bad <= max(2, npix // 20), bad
+        same = (cg == co) & np.all(tg == to.astype(np.float32), axis=1)
+        np.testing.assert_allclose(gg[same], go[same], atol=float(1e-5 * S.max()) + 1e-30)
+        sh2 = np.sum(_hh(sigma, T, m) ** 2)
+        assert np.all(np.abs(ag[same] - ao[same]) <= 1e-5 * S[same, None] / sh2 + 1e-6)
+        assert np.all((ag >= 0) & (ag <= 1)) and np.all(cg <= K)
+
+
+def test_init_depths_edge_cases(gpu, oracle_mod):
+    """Flat zero sketch -> no picks (A14 fill); K larger than the peaks; invalid args write nothing."""
+    import torch
+
+    T, m, N = 1024, 8, 256
+    z = torch.zeros((5, m), dtype=torch.complex64, device="cuda")
+    t, g, a, c = gpu.srt3d_init_depths(z, 1.0, T, N, 4, 10)
+    torch.cuda.synchronize()
+    assert np.all(c.cpu().numpy() == 0) and np.all(t.cpu().numpy() == T / 2) and np.all(a.cpu().numpy() == 0)
+    for bad in (dict(N=2), dict(N=5000), dict(K=0), dict(K=9)):
+        kw = dict(N=N, K=3)
+        kw.update(bad)
+        with pytest.raises(gpu.Srt3dError):
+            gpu.srt3d_init_depths(z, 1.0, T, kw["N"], kw["K"], 10)
+    with pytest.raises(gpu.Srt3dError):
+        gpu.srt3d_backproject(z, 1.0, T, 9000)
+
+
+@pytest.mark.parametrize("T,m,sigma", [(4613, 10, 5.0), (8192, 32, 6.0), (1024, 4, 2.0), (2500, 64, 0.0)])
+def test_init_k1_parity(gpu, oracle_mod, inputs_mod, T, m, sigma):
+    import torch
+
+    rng = np.random.default_rng(T)
+    npix = 500
+    t = rng.uniform(0, T, (npix, 1)).astype(np.float32)
+    t[:4, 0] = [0.0, T - 0.001, T / 2, 1e-3]
+    a = rng.uniform(0.05, 1, (npix, 1)).astype(np.float32)
+    z_a = gpu.srt3d_expected_sketch(_dev(t), _dev(a), sigma, T, m)
+    bins, offs = inputs_mod.random_csr(npix=npix, T=T, max_n=300, seed=T + 1)
+    z_b = _gpu_sketch(gpu, bins, offs, T, m)
+    for z in (z_a, z_b):
+        tg, ag = gpu.srt3d_init_k1(z, sigma, T)
+        torch.cuda.synchronize()
+        zh = z.cpu().numpy()
+        to, ao = oracle_mod.init_k1(zh, sigma, T)
+        tg, ag = tg.cpu().numpy()[:, 0], ag.cpu().numpy()[:, 0]
+        d = np.abs(tg.astype(np.float64) - to)
+        d = np.minimum(d, T - d)
+        ulp = np.spacing(np.float32(T))
+        assert np.all(d <= 0.5 * ulp + 1e-9), float(d.max())
+        assert np.all((tg >= 0) & (tg < T))
+        h = _hh(sigma, T, m)
+        Sa = np.sum(h * np.abs(zh), axis=1) / np.sum(h**2)
+        assert np.all(np.abs(ag - ao) <= 1e-4 * Sa + 1e-7), float(np.abs(ag - ao).max())
+    # noiseless truth is recovered (z_a): t within 0.01 bins, alpha within 1e-4
+    tg, ag = gpu.srt3d_init_k1(z_a, sigma, T)
+    d = np.abs(tg.cpu().numpy() - t)
+    assert np.all(np.minimum(d, T - d) < 0.01)
+    np.testing.assert_allclose(ag.cpu().numpy(), a, atol=1e-4)
