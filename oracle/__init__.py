@@ -49,9 +49,12 @@ def _load():
         lib.srt3d_ref_backproject.argtypes = [P, i64, f64, u32, u32, u32, P]
         lib.srt3d_ref_init_depths.argtypes = [P, i64, f64, u32, u32, u32, u32, u32, P, P, P, P]
         lib.srt3d_ref_init_k1.argtypes = [P, i64, f64, u32, u32, P, P]
+        lib.srt3d_ref_sketch_merge.argtypes = [P, P, P, P, i64, u32, P, P]
+        lib.srt3d_ref_bucket_events.argtypes = [P, P, ctypes.c_uint64, i64, P, P, P]
         for f in ("srt3d_ref_sketch", "srt3d_ref_phase_index", "srt3d_ref_expected_sketch",
                   "srt3d_ref_sketch_grad", "srt3d_ref_descent_update", "srt3d_ref_backproject",
-                  "srt3d_ref_init_depths", "srt3d_ref_init_k1"):
+                  "srt3d_ref_init_depths", "srt3d_ref_init_k1", "srt3d_ref_sketch_merge",
+                  "srt3d_ref_bucket_events"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -172,6 +175,31 @@ def init_k1(z, sigma: float, T: int):
     a = np.zeros(npix)
     _check(_load().srt3d_ref_init_k1(_ptr(zd), npix, float(sigma), T, m, _ptr(t), _ptr(a)), "srt3d_ref_init_k1")
     return t, a
+
+
+def sketch_merge(za, na, zb, nb):
+    """NEXT-4: count-weighted mean of two sketch frames; returns (z complex128 (npix, m), n uint64)."""
+    a, b = _zd(za), _zd(zb)
+    npix, m = a.shape[0], a.shape[1]
+    na = np.ascontiguousarray(na, dtype=np.uint32)
+    nb = np.ascontiguousarray(nb, dtype=np.uint32)
+    z = np.zeros((npix, m, 2))
+    n = np.zeros(npix, dtype=np.uint64)
+    _check(_load().srt3d_ref_sketch_merge(_ptr(a), _ptr(na), _ptr(b), _ptr(nb), npix, m, _ptr(z), _ptr(n)),
+           "srt3d_ref_sketch_merge")
+    return z[..., 0] + 1j * z[..., 1], n
+
+
+def bucket_events(pix, bins, npix: int):
+    """NEXT-4: stable counting sort of (pixel, bin) events -> (offsets uint32 (npix+1,), bins uint16, dropped)."""
+    pix = np.ascontiguousarray(pix, dtype=np.uint32)
+    bins = np.ascontiguousarray(bins, dtype=np.uint16)
+    offs = np.zeros(npix + 1, dtype=np.uint32)
+    out = np.zeros(max(bins.size, 1), dtype=np.uint16)
+    dropped = np.zeros(1, dtype=np.uint64)
+    _check(_load().srt3d_ref_bucket_events(_ptr(pix), _ptr(bins), bins.size, npix, _ptr(offs), _ptr(out),
+                                           _ptr(dropped)), "srt3d_ref_bucket_events")
+    return offs, out[: int(offs[-1])], int(dropped[0])
 
 
 def set_threads(n: int) -> None:

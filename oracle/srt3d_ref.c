@@ -31,6 +31,11 @@
  *   srt3d_ref_init_k1          NEXT-3 K = 1 closed form: depth from the phase
  *                              of z_1, intensity by K = 1 least squares
  *                              (A20).
+ *   srt3d_ref_sketch_merge     NEXT-4 count-weighted mean of two sketches
+ *                              (the online update of P:65).
+ *   srt3d_ref_bucket_events    NEXT-4 stable counting sort of an unsorted
+ *                              (pixel, bin) event stream into the CSR frame
+ *                              srt3d_ref_sketch consumes (A21).
  *
  * Everything is computed in double precision with the textbook formula, in
  * the order the definition states; OpenMP only splits independent pixels.
@@ -354,6 +359,46 @@ int srt3d_ref_init_k1(const double* z, int64_t npix, double sigma, uint32_t T, u
     t_out[i] = t;
     alpha_out[i] = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);
   }
+  return REF_OK;
+}
+
+/* ---- NEXT-4: streaming acquisition (A21) ---- */
+
+/* z = (n_a z_a + n_b z_b) / (n_a + n_b), n = n_a + n_b per pixel;
+ * n = 0 -> z = 0.  z_* are [npix][m][2]. */
+int srt3d_ref_sketch_merge(const double* za, const uint32_t* na, const double* zb, const uint32_t* nb,
+                           int64_t npix, uint32_t m, double* z, uint64_t* n) {
+  if (m < 1 || npix < 0) return REF_EINVAL;
+  for (int64_t i = 0; i < npix; i++) {
+    uint64_t nn = (uint64_t)na[i] + (uint64_t)nb[i];
+    n[i] = nn;
+    for (uint32_t j = 0; j < 2 * m; j++) {
+      size_t o = (size_t)i * 2 * m + j;
+      z[o] = nn ? ((double)na[i] * za[o] + (double)nb[i] * zb[o]) / (double)nn : 0.0;
+    }
+  }
+  return REF_OK;
+}
+
+/* Stable counting sort by pixel: offsets[i] = number of events with pixel < i
+ * (offsets[npix] = kept events); bins_out lists each pixel's bins in event
+ * order.  Events with pix >= npix are dropped (*dropped counts them). */
+int srt3d_ref_bucket_events(const uint32_t* pix, const uint16_t* bins, uint64_t nev, int64_t npix,
+                            uint32_t* offsets, uint16_t* bins_out, uint64_t* dropped) {
+  if (npix < 0) return REF_EINVAL;
+  uint64_t* cnt = (uint64_t*)calloc((size_t)npix + 1, sizeof(uint64_t));
+  if (!cnt) return REF_ENOMEM;
+  uint64_t drop = 0;
+  for (uint64_t e = 0; e < nev; e++) {
+    if ((int64_t)pix[e] < npix) cnt[pix[e] + 1]++;
+    else drop++;
+  }
+  for (int64_t i = 0; i < npix; i++) cnt[i + 1] += cnt[i];
+  for (int64_t i = 0; i <= npix; i++) offsets[i] = (uint32_t)cnt[i];
+  for (uint64_t e = 0; e < nev; e++)
+    if ((int64_t)pix[e] < npix) bins_out[cnt[pix[e]]++] = bins[e];
+  *dropped = drop;
+  free(cnt);
   return REF_OK;
 }
 

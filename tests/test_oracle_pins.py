@@ -409,3 +409,49 @@ def test_IK_closed_form_k1(oracle_mod):
     assert abs(t[0] - 4612.75) < 1e-9 and 0 <= t[0] < T
     t, a = oracle_mod.init_k1(np.zeros((2, 4), complex), 1.0, T)
     assert np.all(t == 0) and np.all(a == 0)
+
+
+# ------------------------------------------------- NEXT-4 streaming acquisition
+def test_M1_merge_equals_sketch_of_concatenation(oracle_mod):
+    """M1: merge of the sketches of two disjoint lists = sketch of the concatenation
+    (the mean property of Eq. (3)); merge with an empty sketch is the identity; commutative;
+    the online update of P:65 is the n_b = 1 case (photon at 0 then T/2 -> z_1 = 0)."""
+    rng = np.random.default_rng(11)
+    T, m = 4613, 10
+    la = [rng.integers(0, T, rng.integers(0, 50)) for _ in range(40)]
+    lb = [rng.integers(0, T, rng.integers(0, 50)) for _ in range(40)]
+    def csr(lists):
+        offs = np.zeros(len(lists) + 1, np.uint32)
+        offs[1:] = np.cumsum([len(l) for l in lists])
+        return np.concatenate(lists).astype(np.uint16), offs
+    za = oracle_mod.sketch(*csr(la), T, m)
+    zb = oracle_mod.sketch(*csr(lb), T, m)
+    na = np.array([len(l) for l in la], np.uint32)
+    nb = np.array([len(l) for l in lb], np.uint32)
+    z, n = oracle_mod.sketch_merge(za, na, zb, nb)
+    zc = oracle_mod.sketch(*csr([np.concatenate([a, b]) for a, b in zip(la, lb)]), T, m)
+    np.testing.assert_allclose(z, zc, atol=1e-12)
+    assert np.array_equal(n, na.astype(np.uint64) + nb)
+    z2, _ = oracle_mod.sketch_merge(zb, nb, za, na)
+    np.testing.assert_allclose(z2, z, atol=1e-15)
+    z3, n3 = oracle_mod.sketch_merge(za, na, np.zeros_like(za), np.zeros_like(na))
+    assert np.array_equal(z3, za) and np.array_equal(n3, na)
+    T2 = 100
+    z0 = oracle_mod.sketch(np.array([0], np.uint16), np.array([0, 1], np.uint32), T2, 1)
+    zh = oracle_mod.sketch(np.array([50], np.uint16), np.array([0, 1], np.uint32), T2, 1)
+    zz, nn = oracle_mod.sketch_merge(z0, np.array([1], np.uint32), zh, np.array([1], np.uint32))
+    assert abs(zz[0, 0]) < 1e-15 and nn[0] == 2
+
+
+def test_BK1_bucketing_is_a_stable_sort(oracle_mod):
+    """BK1 (A21): the CSR built from an unsorted event stream equals numpy's stable argsort by
+    pixel (an independent library primitive); out-of-range pixels are dropped and counted."""
+    rng = np.random.default_rng(4)
+    npix, nev = 300, 20000
+    pix = rng.integers(0, npix + 5, nev).astype(np.uint32)
+    bins = rng.integers(0, 4096, nev).astype(np.uint16)
+    offs, out, dropped = oracle_mod.bucket_events(pix, bins, npix)
+    keep = pix < npix
+    order = np.argsort(pix[keep], kind="stable")
+    assert np.array_equal(out, bins[keep][order]) and dropped == int((~keep).sum())
+    assert np.array_equal(offs, np.concatenate([[0], np.cumsum(np.bincount(pix[keep], minlength=npix))]))
