@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-init", action="store_true", help="skip the NEXT-3 initialisation timings")
     ap.add_argument("--init-grid", type=int, default=0, help="backprojection grid points (default 16 m)")
     ap.add_argument("--init-min-sep", type=int, default=50, help="minimum separation of initial depths (bins)")
+    ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 bucketing / merge timings")
     return ap.parse_args()
 
 
@@ -325,6 +326,34 @@ def run_srt3d(args):
         grad_cold_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in times[1:])
         del flush
 
+    # NEXT-4 streaming acquisition on this frame: the frame's photons as an
+    # unsorted event stream (pixel ids shuffled on the GPU) -> CSR, and the
+    # count-weighted merge of the frame's sketch into a running sketch.
+    stream_ms = None
+    if not args.no_stream and f.n_photons < (1 << 31):
+        counts = (pipe.offsets[1:].to(torch.int64) - pipe.offsets[:-1].to(torch.int64))
+        ev_pix = torch.repeat_interleave(torch.arange(f.npix, device="cuda", dtype=torch.int64), counts)
+        perm = torch.randperm(f.n_photons, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
+        ev_pix = ev_pix[perm].to(torch.int32).view(torch.uint32).contiguous()
+        ev_bin = pipe.bins[: f.n_photons].view(torch.int16)[perm].view(torch.uint16).contiguous()
+        del perm, counts
+        n_run = (pipe.offsets[1:].to(torch.int64) - pipe.offsets[:-1].to(torch.int64)).to(torch.int32).view(
+            torch.uint32).contiguous()
+        z_run, n_acc = pipe.z.clone(), n_run.clone()
+        with torch.cuda.stream(s):
+            srt3d.srt3d_bucket_events(ev_pix, ev_bin, f.npix)
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(5)]
+            for e in ev:
+                e[0].record(s)
+                srt3d.srt3d_bucket_events(ev_pix, ev_bin, f.npix)
+                e[1].record(s)
+                srt3d.srt3d_sketch_merge(z_run, n_acc, pipe.z, n_run, z_out=z_run, n_out=n_acc)
+                e[2].record(s)
+        s.synchronize()
+        stream_ms = {"bucket_ms": statistics.median(e[0].elapsed_time(e[1]) for e in ev),
+                     "merge_ms": statistics.median(e[1].elapsed_time(e[2]) for e in ev)}
+        del ev_pix, ev_bin, z_run, n_acc, n_run
+
     # NEXT-3 initialisation kernels on this frame's sketch (outside the timed
     # step, which starts from theta0 = t* + 10 per BASELINE.json): greedy
     # backprojection depths (grid N, K picks) and the K = 1 closed form.
@@ -416,6 +445,19 @@ def run_srt3d(args):
                             "pixels_per_s": f.npix / (init_ms["k1_ms"] * 1e-3),
                             "roofline": roofline("srt3d_init_k1", k_b, k_f, init_ms["k1_ms"])},
                 "note": "NEXT-3, timed outside the step (the step starts from theta0 = t* + 10)"}
+    stream = None
+    if stream_ms is not None:
+        # bucketing: read each (uint32 pixel, uint16 bin) event once, write its bin, write offsets
+        b_b = 8.0 * f.n_photons + 4.0 * (f.npix + 1)
+        # merge: read two sketch rows + counts, write one
+        m_b = f.npix * (3 * 8.0 * f.m + 3 * 4.0)
+        stream = {"bucket_events": {"kernel": "srt3d_bucket_events", "events": f.n_photons, "ms": stream_ms["bucket_ms"],
+                                    "events_per_s": f.n_photons / (stream_ms["bucket_ms"] * 1e-3),
+                                    "roofline": roofline("srt3d_bucket_events", b_b, 0.0, stream_ms["bucket_ms"]),
+                                    "note": "count + scan + scatter; pixel ids read twice, 2 global atomics per event"},
+                  "sketch_merge": {"kernel": "srt3d_sketch_merge", "ms": stream_ms["merge_ms"],
+                                   "roofline": roofline("srt3d_sketch_merge", m_b, 0.0, stream_ms["merge_ms"])},
+                  "note": "NEXT-4, timed outside the step"}
     # dominant kernel (larger share of the step) -> the line's roofline object
     traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -444,6 +486,7 @@ def run_srt3d(args):
             "config": config_obj(f, args), "clocks": clocks, "e2e": e2e,
             "gpu_launches": pipe.launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad, "init": init,
+            "stream": stream,
             "step_definition": "srt3d_sketch over the frame + iters x srt3d_sketch_grad_step (CUDA graphs)"}
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -219,6 +219,37 @@ int srt3d_init_k1(const float* z, int64_t npix, float sigma, uint32_t T, uint32_
                   void* stream);
 
 /*
+ * NEXT-4 — streaming acquisition: the sketch "can be updated in
+ * an online fashion with each incoming photon".
+ *
+ * srt3d_sketch_merge — per pixel z_out = (n_a z_a + n_b z_b) / (n_a + n_b),
+ * n_out = n_a + n_b (n = 0 -> z = 0): folds the sketch of a
+ * new photon batch (n_b = its counts) into a running sketch.
+ *   z_a, z_b, z_out float [npix][m][2] (8-byte aligned); n_a, n_b, n_out
+ *   uint32 [npix].  z_out may alias z_a (or z_b) and n_out may alias n_a (or
+ *   n_b): in-place accumulation.  Precondition: n_a + n_b < 2^32.
+ */
+int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb, int64_t npix,
+                       uint32_t m, float* z_out, uint32_t* n_out, void* stream);
+
+/*
+ * srt3d_bucket_events — an unsorted stream of photon events (pixel index,
+ * bin) into the pixel-sorted CSR frame srt3d_sketch consumes (reading A21):
+ * offsets[i] = number of events with pixel < i, offsets[npix] = kept events,
+ * and each pixel's bins contiguous in bins_out.  Within a pixel the order
+ * follows atomic arrival (a permutation of the stable order; the sketch is
+ * order-invariant up to fp32 rounding).  Events with pixel >= npix are
+ * dropped and counted into *dropped (device uint32, may be NULL).
+ *   pix uint32 [nevents], bins uint16 [nevents] (bins < T is the same
+ *   precondition as for srt3d_sketch), nevents < 2^32; offsets uint32
+ *   [npix+1] and bins_out uint16 [nevents] outputs; scratch uint32
+ *   [srt3d_bucket_scratch_words(npix)] device workspace owned by the caller.
+ */
+int srt3d_bucket_events(const uint32_t* pix, const uint16_t* bins, uint64_t nevents, int64_t npix,
+                        uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch, uint32_t* dropped, void* stream);
+uint64_t srt3d_bucket_scratch_words(int64_t npix);
+
+/*
  * srt3d_check_csr — debug validator (not on the hot path).  Sets *bad (a
  * device int32 the caller zeroes first) to non-zero if some bins[p] >= T or
  * some offsets[i+1] < offsets[i].

@@ -37,7 +37,8 @@ EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex
            "srt3d_sketch_grad",
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
            "srt3d_sketch_plan", "srt3d_fit_pixelwise",
-           "srt3d_backproject", "srt3d_init_depths", "srt3d_init_k1")
+           "srt3d_backproject", "srt3d_init_depths", "srt3d_init_k1", "srt3d_sketch_merge",
+           "srt3d_bucket_events", "srt3d_bucket_scratch_words")
 
 
 class Srt3dError(RuntimeError):
@@ -74,6 +75,10 @@ def load_library(path: str | None = None):
     lib.srt3d_backproject.argtypes = [P, i64, f32, u32, u32, u32, P, P]
     lib.srt3d_init_depths.argtypes = [P, i64, f32, u32, u32, u32, u32, u32, P, P, P, P, P]
     lib.srt3d_init_k1.argtypes = [P, i64, f32, u32, u32, P, P, P]
+    lib.srt3d_sketch_merge.argtypes = [P, P, P, P, i64, u32, P, P, P]
+    lib.srt3d_bucket_events.argtypes = [P, P, u64, i64, P, P, P, P, P]
+    lib.srt3d_bucket_scratch_words.argtypes = [i64]
+    lib.srt3d_bucket_scratch_words.restype = u64
     for f in EXPORTS[2:]:
         getattr(lib, f).restype = ctypes.c_int
     if path is None:
@@ -219,6 +224,36 @@ def srt3d_init_k1(z, sigma: float, T: int, stream=None):
     _need_cuda(z)
     _call("srt3d_init_k1", _ptr(z), npix, float(sigma), T, m, _ptr(t), _ptr(a), _stream(stream))
     return t, a
+
+
+def srt3d_sketch_merge(za, na, zb, nb, z_out=None, n_out=None, stream=None):
+    """NEXT-4: count-weighted mean of two sketch frames (in place when z_out is za / n_out is na)."""
+    npix, m = za.shape
+    z_out = torch.empty_like(za) if z_out is None else z_out
+    n_out = torch.empty_like(na) if n_out is None else n_out
+    _need_cuda(za, na, zb, nb, z_out, n_out)
+    _call("srt3d_sketch_merge", _ptr(za), _ptr(na), _ptr(zb), _ptr(nb), npix, m, _ptr(z_out), _ptr(n_out),
+          _stream(stream))
+    return z_out, n_out
+
+
+def srt3d_bucket_scratch_words(npix: int) -> int:
+    """uint32 words of device workspace srt3d_bucket_events needs for npix pixels."""
+    return int(load_library().srt3d_bucket_scratch_words(int(npix)))
+
+
+def srt3d_bucket_events(pix, bins, npix: int, stream=None):
+    """NEXT-4: unsorted (pixel uint32, bin uint16) events -> CSR (offsets uint32, bins uint16, dropped)."""
+    dev = pix.device
+    nev = pix.numel()
+    offsets = torch.empty(npix + 1, dtype=torch.uint32, device=dev)
+    out = torch.empty(max(nev, 1), dtype=torch.uint16, device=dev)
+    scratch = torch.empty(srt3d_bucket_scratch_words(npix), dtype=torch.uint32, device=dev)
+    dropped = torch.empty(1, dtype=torch.uint32, device=dev)
+    _need_cuda(pix, bins)
+    _call("srt3d_bucket_events", _ptr(pix), _ptr(bins), nev, int(npix), _ptr(offsets), _ptr(out), _ptr(scratch),
+          _ptr(dropped), _stream(stream))
+    return offsets, out, dropped
 
 
 def srt3d_check_csr(bins, offsets, T: int, stream=None) -> int:

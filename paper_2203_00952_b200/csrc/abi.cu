@@ -369,6 +369,42 @@ int srt3d_init_k1(const float* z, int64_t npix, float sigma, uint32_t T, uint32_
   return SRT3D_OK;
 }
 
+// ---- NEXT-4 streaming acquisition -------------------------------------------
+int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb, int64_t npix,
+                       uint32_t m, float* z_out, uint32_t* n_out, void* stream) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  if (m < 1) return fail(SRT3D_EINVAL, "m=%u < 1", m);
+  if (m > SRT3D_MAX_M) return fail(SRT3D_EUNSUPPORTED, "m=%u exceeds SRT3D_MAX_M=%u", m, SRT3D_MAX_M);
+  if (npix == 0) return SRT3D_OK;
+  if (!za || !na || !zb || !nb || !z_out || !n_out) return fail(SRT3D_ENULL, "all pointers must be non-NULL");
+  if (!aligned(za, 8) || !aligned(zb, 8) || !aligned(z_out, 8) || !aligned(na, 4) || !aligned(nb, 4) ||
+      !aligned(n_out, 4))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and n 4-byte aligned");
+  cudaError_t e = srt3d::launch_merge(za, na, zb, nb, npix, m, z_out, n_out, (cudaStream_t)stream,
+                                      num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch_merge");
+  return SRT3D_OK;
+}
+
+uint64_t srt3d_bucket_scratch_words(int64_t npix) {
+  return npix < 0 ? 0 : (uint64_t)srt3d::bucket_scratch_words(npix);
+}
+
+int srt3d_bucket_events(const uint32_t* pix, const uint16_t* bins, uint64_t nevents, int64_t npix,
+                        uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch, uint32_t* dropped, void* stream) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  if (nevents >= (1ull << 32)) return fail(SRT3D_EINVAL, "nevents=%llu must be < 2^32", (unsigned long long)nevents);
+  if (!offsets || !scratch) return fail(SRT3D_ENULL, "offsets/scratch must be non-NULL");
+  if (nevents && (!pix || !bins || !bins_out)) return fail(SRT3D_ENULL, "pix/bins/bins_out must be non-NULL");
+  if (!aligned(pix, 4) || !aligned(bins, 2) || !aligned(offsets, 4) || !aligned(bins_out, 2) ||
+      !aligned(scratch, 4) || (dropped && !aligned(dropped, 4)))
+    return fail(SRT3D_EALIGN, "pix/offsets/scratch/dropped 4-byte and bins 2-byte aligned");
+  cudaError_t e = srt3d::launch_bucket(pix, bins, nevents, npix, offsets, bins_out, scratch, dropped,
+                                       (cudaStream_t)stream, num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_bucket_events");
+  return SRT3D_OK;
+}
+
 int srt3d_check_csr(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, int32_t* bad,
                     void* stream) {
   if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);

@@ -1,0 +1,119 @@
+"""NEXT-4 GPU <-> oracle parity: sketch merge and event bucketing
+through the C ABI.
+
+  * bucketing: offsets bit-exact; each pixel's bin multiset bit-exact (the order
+    inside a pixel follows atomic arrival: several orders are correct, the
+    multiset is unique); dropped-event count exact.
+  * events -> CSR -> srt3d_sketch: |delta| <= 1e-5 per component vs the oracle's
+    sketch of its own (stable) CSR (Eq. (3) is order-invariant; fp32 rounding
+    order differs).
+  * merge: |delta| <= 2e-7 * (|z_a| + |z_b|) + 1e-12 per component (weights
+    rounded once to fp32, one FMA + one product).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _events(npix, T, n_ev, seed, extra_bad=0):
+    rng = np.random.default_rng(seed)
+    w = rng.exponential(1.0, npix)
+    w[rng.random(npix) < 0.1] = 0.0  # empty pixels
+    p = rng.choice(npix, size=n_ev, p=w / w.sum()).astype(np.uint32)
+    if extra_bad:
+        p[rng.choice(n_ev, extra_bad, replace=False)] = npix + rng.integers(0, 7, extra_bad)
+    b = rng.integers(0, T, n_ev).astype(np.uint16)
+    return p, b
+
+
+@pytest.mark.parametrize("npix,T,n_ev,bad", [(1000, 4096, 200000, 0), (262144, 8192, 1000000, 17),
+                                             (5000, 1024, 0, 0), (1, 100, 5000, 3), (70000, 2500, 300000, 0)])
+def test_bucket_events_parity(gpu, oracle_mod, npix, T, n_ev, bad):
+    import torch
+
+    p, b = _events(npix, T, n_ev, seed=npix + n_ev, extra_bad=bad)
+    offs, out, dropped = gpu.srt3d_bucket_events(_dev(p), _dev(b), npix)
+    torch.cuda.synchronize()
+    oo, ob, od = oracle_mod.bucket_events(p, b, npix)
+    offs = offs.cpu().numpy()
+    assert np.array_equal(offs, oo) and int(dropped.item()) == od == bad
+    out = out.cpu().numpy()[: int(oo[-1])]
+    # per-pixel multisets: sort inside every segment (keys: pixel, then bin)
+    seg = np.repeat(np.arange(npix), np.diff(oo.astype(np.int64)))
+    assert np.array_equal(out[np.lexsort((out, seg))], ob[np.lexsort((ob, seg))])
+
+
+@pytest.mark.parametrize("T,m", [(8192, 32), (4613, 10), (1024, 4)])
+def test_events_to_sketch(gpu, oracle_mod, T, m):
+    import torch
+
+    npix = 3000
+    p, b = _events(npix, T, 600000, seed=T)
+    offs, out, _ = gpu.srt3d_bucket_events(_dev(p), _dev(b), npix)
+    z = gpu.srt3d_sketch(out, offs, T, m, total_photons=len(p))
+    torch.cuda.synchronize()
+    oo, ob, _ = oracle_mod.bucket_events(p, b, npix)
+    zo = oracle_mod.sketch(ob, oo, T, m)
+    zg = z.cpu().numpy()
+    assert max(np.abs(zg.real - zo.real).max(), np.abs(zg.imag - zo.imag).max()) <= 1e-5
+
+
+@pytest.mark.parametrize("m", [1, 10, 32, 64])
+def test_sketch_merge_parity(gpu, oracle_mod, inputs_mod, m):
+    """Random sketches and counts (incl. zero counts); out of place, then in place (z_out = z_a,
+    n_out = n_a) — bitwise equal; merging two batch sketches equals the sketch of the union."""
+    import torch
+
+    rng = np.random.default_rng(m)
+    npix = 5001
+    za = (rng.normal(size=(npix, m)) + 1j * rng.normal(size=(npix, m))).astype(np.complex64)
+    zb = (rng.normal(size=(npix, m)) + 1j * rng.normal(size=(npix, m))).astype(np.complex64)
+    na = rng.integers(0, 3000, npix).astype(np.uint32)
+    nb = rng.integers(0, 3000, npix).astype(np.uint32)
+    na[:7] = 0
+    nb[3:9] = 0
+    zo, no = oracle_mod.sketch_merge(za, na, zb, nb)
+    da, db, dna, dnb = _dev(za), _dev(zb), _dev(na), _dev(nb)
+    z1, n1 = gpu.srt3d_sketch_merge(da, dna, db, dnb)
+    torch.cuda.synchronize()
+    z1h = z1.cpu().numpy()
+    tol = 2e-7 * (np.abs(za) + np.abs(zb)) + 1e-12
+    assert np.all(np.abs(z1h.real - zo.real) <= tol) and np.all(np.abs(z1h.imag - zo.imag) <= tol)
+    assert np.array_equal(n1.cpu().numpy().astype(np.uint64), no)
+    gpu.srt3d_sketch_merge(da, dna, db, dnb, z_out=da, n_out=dna)
+    torch.cuda.synchronize()
+    assert np.array_equal(da.cpu().numpy().view(np.uint64), z1h.view(np.uint64))
+    assert np.array_equal(dna.cpu().numpy(), n1.cpu().numpy())
+    # streaming: sketch of batch A merged with sketch of batch B == sketch of A u B
+    T = 4096
+    b1, o1 = inputs_mod.random_csr(npix=400, T=T, max_n=500, seed=1)
+    b2, o2 = inputs_mod.random_csr(npix=400, T=T, max_n=500, seed=2)
+    s1 = gpu.srt3d_sketch(_dev(b1), _dev(o1), T, m, total_photons=int(o1[-1]))
+    s2 = gpu.srt3d_sketch(_dev(b2), _dev(o2), T, m, total_photons=int(o2[-1]))
+    zm, nm = gpu.srt3d_sketch_merge(s1, _dev(np.diff(o1.astype(np.int64)).astype(np.uint32)), s2,
+                                    _dev(np.diff(o2.astype(np.int64)).astype(np.uint32)))
+    torch.cuda.synchronize()
+    lists = [np.concatenate([b1[o1[i]:o1[i + 1]], b2[o2[i]:o2[i + 1]]]) for i in range(400)]
+    ou = np.zeros(401, np.uint32)
+    ou[1:] = np.cumsum([len(x) for x in lists])
+    zu = oracle_mod.sketch(np.concatenate(lists).astype(np.uint16), ou, T, m)
+    zmh = zm.cpu().numpy()
+    assert max(np.abs(zmh.real - zu.real).max(), np.abs(zmh.imag - zu.imag).max()) <= 1e-5
+    assert np.array_equal(nm.cpu().numpy(), np.diff(ou.astype(np.int64)).astype(np.uint32))
+
+
+def test_stream_errors(gpu):
+    import torch
+
+    n = torch.zeros(4, dtype=torch.uint32, device="cuda")
+    z65 = torch.zeros((4, 65), dtype=torch.complex64, device="cuda")
+    with pytest.raises(gpu.Srt3dError):
+        gpu.srt3d_sketch_merge(z65, n, z65, n)  # m > SRT3D_MAX_M
+    assert gpu.srt3d_bucket_scratch_words(262144) >= 262144
