@@ -159,7 +159,7 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   for (uint32_t j0 = 0; j0 < m; j0 += 32) {
     a.j0 = j0;
     const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
-    cudaError_t e = path == SRT3D_PATH_BINCOUNT ? srt3d::launch_sketch_hist(M, a, s, nsm)
+    cudaError_t e = path == SRT3D_PATH_BINCOUNT ? srt3d::launch_sketch_hist(M, a, mean, s, nsm)
                     : path == SRT3D_PATH_PAIRED ? srt3d::launch_sketch_pair(M, a, s, nsm)
                                                 : srt3d::launch_sketch_pass(M, G, a, s, nsm);
     if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");

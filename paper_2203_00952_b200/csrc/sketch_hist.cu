@@ -10,11 +10,13 @@
 //   2. stream the pixel's photons with 16-byte vector loads (8 in flight per
 //      thread) and count them with shared-memory atomics — 2 B of HBM per
 //      photon, no FP32 work: this is the HBM-bound phase;
-//   3. DFT of the histogram: thread t takes bins x = t, t+B, ..., weight
-//      h[x] * tab[x], then the packed complex recurrence over j (T*M terms per
-//      pixel instead of n*M);
+//   3. DFT of the histogram: thread t takes bins x = t, t+B, ..., weight h[x],
+//      rotated Chebyshev recurrence over j with the bin's rotation class
+//      known per branch (T*M terms per pixel instead of n*M; 1 FFMA2 + 1 FADD2
+//      per term, DESIGN.md §5.0/§5.3);
 //   4. fixed-order block reduction (warp reduce-scatter + smem), scale by 1/n.
 #include <cstdint>
+#include <utility>
 
 #include "sketch_impl.cuh"
 
@@ -24,6 +26,36 @@ namespace srt3d {
 #define HS_DEFAULT_THREADS 512  // CTA size (tools/hist_tune.cu)
 #define HS_DEFAULT_UNROLL 8     // 16-byte loads in flight per thread
 #endif
+
+// acc[J] += h * e^{i 2 pi (j0 + 1 + J) x / T}, J < M, by the rotated
+// Chebyshev chain of bin x (ROT: class B, chain on i*w, rotated back).
+template <int M, bool ROT, int J>
+__device__ __forceinline__ void dft_term(u64 (&acc)[M], Chain& c) {
+  if constexpr (J > 0) c.advance();
+  acc[J] = fadd2(acc[J], ROT ? rot_back<J>(c.B) : c.B);
+}
+template <int M, bool ROT, int... J>
+__device__ __forceinline__ void dft_terms(u64 (&acc)[M], Chain& c, std::integer_sequence<int, J...>) {
+  (dft_term<M, ROT, J>(acc, c), ...);
+}
+template <int M, bool ROT>
+__device__ __forceinline__ void dft_bin(u64 (&acc)[M], const float2* tab, uint32_t x, float h, uint32_t T,
+                                        uint32_t j0, float invT) {
+  const float2 w = tab[x];
+  Chain c;
+  const float cc = ROT ? -2.f * w.y : 2.f * w.x;  // 2 cos(theta'), theta' = theta (+ pi/2)
+  c.C2 = pk(cc, cc);
+  if (j0 == 0) {
+    c.A = pk(h, 0.f);
+    c.B = ROT ? pk(-h * w.y, h * w.x) : pk(h * w.x, h * w.y);
+  } else {  // j0 = 32, 64, ...: i^{j0} = 1, i^{j0+1} = i
+    const float2 a0 = tab[phase_index(x, j0, T, invT)];
+    const float2 a1 = tab[phase_index(x, j0 + 1, T, invT)];
+    c.A = pk(h * a0.x, h * a0.y);
+    c.B = ROT ? pk(-h * a1.y, h * a1.x) : pk(h * a1.x, h * a1.y);
+  }
+  dft_terms<M, ROT>(acc, c, std::make_integer_sequence<int, M>{});
+}
 
 template <int M, int HS_THREADS, int HS_UNROLL>
 __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
@@ -60,7 +92,8 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
     const int nh = (int)(hend - beg), nt = (int)(end - tbeg);
     if (tid < nh) atomicAdd(&hist[bins[beg + tid]], 1u);
     else if (tid < nh + nt) atomicAdd(&hist[bins[tbeg + (tid - nh)]], 1u);
-    // body: 16-byte chunks, HS_UNROLL loads in flight per thread
+    // 16-byte chunks, HS_UNROLL loads in flight per thread: full rounds, then
+    // one predicated round (any photon count keeps its loads in flight)
     long long c = cb + tid;
     for (; c + (HS_UNROLL - 1) * HS_THREADS < ce; c += HS_UNROLL * HS_THREADS) {
       uint4 v[HS_UNROLL];
@@ -76,38 +109,39 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
         }
       }
     }
-    for (; c < ce; c += HS_THREADS) {
-      const uint4 v = __ldcs(vb + c);
-      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+    if (c < ce) {
+      uint4 v[HS_UNROLL];
 #pragma unroll
-      for (int h = 0; h < 4; h++) {
-        atomicAdd(&hist[w4[h] & 0xffffu], 1u);
-        atomicAdd(&hist[w4[h] >> 16], 1u);
+      for (int u = 0; u < HS_UNROLL; u++)
+        v[u] = c + u * HS_THREADS < ce ? __ldcs(vb + c + u * HS_THREADS) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < HS_UNROLL; u++) {
+        if (c + u * HS_THREADS >= ce) break;
+        const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+          atomicAdd(&hist[w4[h] & 0xffffu], 1u);
+          atomicAdd(&hist[w4[h] >> 16], 1u);
+        }
       }
     }
     __syncthreads();
 
-    // DFT of the histogram over this thread's bins
+    // DFT of the histogram over this thread's bins: the rotated Chebyshev
+    // recurrence (one FFMA2 per term).  The rotation class of bin x is a
+    // function of x, so each branch below is class-uniform and its
+    // back-rotation is a compile-time operand swizzle; consecutive bins share
+    // a class except at four boundaries, so warps almost never diverge.
     u64 acc[M];
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = 0ull;
     for (uint32_t x = tid; x < T; x += HS_THREADS) {
       const float h = (float)hist[x];
       hist[x] = 0u;  // ready for the next pixel
-      const float2 w = tab[x];
-      const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
-      u64 P = W;
-      if (j0) {
-        const float2 an = tab[phase_index(x, j0 + 1, T, invT)];
-        P = pk(an.x, an.y);
-      }
-      P = fmul2(pk(h, h), P);
-      acc[0] = fadd2(acc[0], P);
-#pragma unroll
-      for (int j = 1; j < M; j++) {
-        P = cmul2(P, W, Wn);
-        acc[j] = fadd2(acc[j], P);
-      }
+      if (class_b(x, T))
+        dft_bin<M, true>(acc, tab, x, h, T, j0, invT);
+      else
+        dft_bin<M, false>(acc, tab, x, h, T, j0, invT);
     }
     float f[NVP];
 #pragma unroll
@@ -162,11 +196,22 @@ static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sm
 #ifndef HS_NO_DISPATCH
 size_t sketch_hist_smem(uint32_t T, int M) { return sketch_hist_smem_t(T, M, 512); }  // largest CTA variant
 
-cudaError_t launch_sketch_hist(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
+// CTA size by the mean photons per pixel (tools/hist_tune.cu on B200): large
+// CTAs stream heavy pixels (n ~ 1e5-1e6) best; for n ~ 1e4 the per-pixel DFT,
+// reduction and barriers dominate and more, smaller CTAs per SM win (C3-like
+// frame: 512 threads 1.37 ms, 128 threads 0.86 ms).
+template <int M>
+static cudaError_t launch_hist_m(const SketchArgs& a, double mean, cudaStream_t s, int num_sms) {
+  if (mean < 3.0e4) return launch_hist_t<M, 128, 4>(a, s, num_sms);
+  if (mean < 8.0e4) return launch_hist_t<M, 256, 8>(a, s, num_sms);
+  return launch_hist_t<M, 512, 8>(a, s, num_sms);
+}
+
+cudaError_t launch_sketch_hist(int M, const SketchArgs& a, double mean_photons, cudaStream_t s, int num_sms) {
   switch (M) {
 #define SRT3D_CASE(MM) \
   case MM:             \
-    return launch_hist_t<MM>(a, s, num_sms);
+    return launch_hist_m<MM>(a, mean_photons, s, num_sms);
     SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
     SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
     SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)

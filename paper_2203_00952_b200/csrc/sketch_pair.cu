@@ -36,39 +36,6 @@ namespace srt3d {
 constexpr int PQ_CAP = 512;                  // photons per class queue per warp (power of two)
 constexpr int PQ_SMEM_PER_WARP = 2 * (PQ_CAP + 8) * 2;  // + junk slots
 
-// Class of bin x: true = B (|sin theta| < |cos theta|, chain on theta + pi/2).
-__device__ __forceinline__ bool class_b(uint32_t x, uint32_t T) {
-  uint32_t u = 2u * x;
-  u = u >= T ? u - T : u;  // 2x mod T (x < T)
-  return 4u * u < T || 4u * u > 3u * T;
-}
-
-// Rotation of a class-B term back by (-i)^{1+J}: a compile-time operand
-// swizzle / negation of the consuming FADD2.
-template <int J>
-__device__ __forceinline__ u64 rot_back(u64 y) {
-  constexpr int rot = (1 + J) & 3;
-  if constexpr (rot == 0) {
-    return y;
-  } else if constexpr (rot == 1) {  // (-i) v = (s, -c)
-    return pk(hi_of(y), -lo_of(y));
-  } else if constexpr (rot == 2) {
-    return neg2(y);
-  } else {  // (+i) v = (-s, c)
-    return pk(-hi_of(y), lo_of(y));
-  }
-}
-
-// One rotated Chebyshev chain: (A, B) = (v_{j-1}, v_j), C2 = (2 cos theta')^2.
-struct Chain {
-  u64 A, B, C2;
-  __device__ __forceinline__ void advance() {
-    const u64 N = ffma2(B, C2, neg2(A));
-    A = B;
-    B = N;
-  }
-};
-
 template <int M>
 struct PairAcc {
   u64 acc[M];

@@ -1,6 +1,7 @@
 // Tuning harness (tools only) for the bin-count sketch kernel: CTA size and
-// loads in flight, on a C4-shaped frame (64x64 px, T=4096, m=10, n photons per
-// pixel, half of them in a 17-bin cluster).
+// loads in flight, on C3-like (256x256 px, T=2500, m=20, n=1e4) and C4-shaped
+// frames (64x64 px, T=4096, m=10, n photons per pixel), half of the photons of
+// a pixel in a 17-bin cluster.
 #define HS_NO_DISPATCH
 #include "../paper_2203_00952_b200/csrc/sketch_hist.cu"
 #include <cstdio>
@@ -15,19 +16,19 @@ using namespace srt3d;
       exit(1);                                                          \
     }                                                                   \
   } while (0)
-template <int NT, int UNR>
+template <int M, int NT, int UNR>
 void run(const SketchArgs& a, int nsm, double photons, const char* tag) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   {
-    cudaError_t ee = launch_hist_t<10, NT, UNR>(a, 0, nsm);
+    cudaError_t ee = launch_hist_t<M, NT, UNR>(a, 0, nsm);
     CK(ee);
   }
   CK(cudaDeviceSynchronize());
   cudaEventRecord(e0);
   for (int r = 0; r < 5; r++) {
-    cudaError_t ee = launch_hist_t<10, NT, UNR>(a, 0, nsm);
+    cudaError_t ee = launch_hist_t<M, NT, UNR>(a, 0, nsm);
     CK(ee);
   }
   cudaEventRecord(e1);
@@ -42,9 +43,10 @@ void run(const SketchArgs& a, int nsm, double photons, const char* tag) {
 int main() {
   int nsm;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-  for (long long n : {100000LL, 1000000LL}) {
-    const long long npix = 4096;
-    const uint32_t T = 4096;
+  struct F { long long npix, n; uint32_t T; const char* tag; };
+  for (F fr : {F{65536, 10000, 2500, "C3like"}, F{4096, 10000, 4096, "C4@1e4"}, F{4096, 100000, 4096, "C4@1e5"}}) {
+    const long long npix = fr.npix, n = fr.n;
+    const uint32_t T = fr.T;
     std::vector<uint16_t> bins((size_t)npix * n);
     std::mt19937_64 g(7);
     for (long long i = 0; i < npix; i++) {
@@ -61,20 +63,24 @@ int main() {
     float* dz;
     CK(cudaMalloc(&db, bins.size() * 2));
     CK(cudaMalloc(&dof, offs.size() * 4));
-    CK(cudaMalloc(&dz, npix * 10 * 8));
+    CK(cudaMalloc(&dz, npix * 32 * 8));
     CK(cudaMemcpy(db, bins.data(), bins.size() * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dof, offs.data(), offs.size() * 4, cudaMemcpyHostToDevice));
-    SketchArgs a{db, dof, npix, T, 0, 10u, dz};
-    const char* tag = n == 100000 ? "C4@1e5" : "C4@1e6";
     double ph = (double)npix * n;
-    run<512, 4>(a, nsm, ph, tag);
-    run<512, 8>(a, nsm, ph, tag);
-    run<256, 4>(a, nsm, ph, tag);
-    run<256, 8>(a, nsm, ph, tag);
-    run<1024, 2>(a, nsm, ph, tag);
-    run<1024, 4>(a, nsm, ph, tag);
-    run<128, 8>(a, nsm, ph, tag);
-    run<512, 2>(a, nsm, ph, tag);
+    if (T == 2500) {
+      SketchArgs a{db, dof, npix, T, 0, 20u, dz};
+      run<20, 512, 8>(a, nsm, ph, fr.tag);
+      run<20, 256, 8>(a, nsm, ph, fr.tag);
+      run<20, 128, 8>(a, nsm, ph, fr.tag);
+      run<20, 128, 4>(a, nsm, ph, fr.tag);
+      run<20, 64, 8>(a, nsm, ph, fr.tag);
+    } else {
+      SketchArgs a{db, dof, npix, T, 0, 10u, dz};
+      run<10, 512, 8>(a, nsm, ph, fr.tag);
+      run<10, 256, 8>(a, nsm, ph, fr.tag);
+      run<10, 128, 8>(a, nsm, ph, fr.tag);
+      run<10, 1024, 4>(a, nsm, ph, fr.tag);
+    }
     cudaFree(db);
     cudaFree(dof);
     cudaFree(dz);
