@@ -354,6 +354,23 @@ def run_srt3d(args):
                      "merge_ms": statistics.median(e[1].elapsed_time(e[2]) for e in ev)}
         del ev_pix, ev_bin, z_run, n_acc, n_run
 
+    # NEXT-2 fused pixelwise fit: the step's `iters` data steps in ONE launch
+    # (z staged once, theta in registers; bitwise equal to the iterated steps)
+    fit_ms = None
+    if f.iters > 0:
+        tt, aa = pipe.t0.clone(), pipe.a0.clone()
+        with torch.cuda.stream(s):
+            srt3d.srt3d_fit_pixelwise(pipe.z, tt, aa, f.sigma, f.T, f.m, f.iters)
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(3)]
+            for e in ev:
+                tt.copy_(pipe.t0)
+                aa.copy_(pipe.a0)
+                e[0].record(s)
+                srt3d.srt3d_fit_pixelwise(pipe.z, tt, aa, f.sigma, f.T, f.m, f.iters)
+                e[1].record(s)
+        s.synchronize()
+        fit_ms = statistics.median(e[0].elapsed_time(e[1]) for e in ev)
+
     # NEXT-3 initialisation kernels on this frame's sketch (outside the timed
     # step, which starts from theta0 = t* + 10 per BASELINE.json): greedy
     # backprojection depths (grid N, K picks) and the K = 1 closed form.
@@ -445,6 +462,16 @@ def run_srt3d(args):
                             "pixels_per_s": f.npix / (init_ms["k1_ms"] * 1e-3),
                             "roofline": roofline("srt3d_init_k1", k_b, k_f, init_ms["k1_ms"])},
                 "note": "NEXT-3, timed outside the step (the step starts from theta0 = t* + 10)"}
+    fit = None
+    if fit_ms is not None:
+        # same arithmetic per pixel-iteration as the step (F below); bytes: z and theta once per launch
+        f_f = f.iters * f.npix * (21.0 * f.K * f.m + 7.0 * f.m + 3.0 * f.K)
+        f_b = f.npix * (8.0 * f.m + 16.0 * f.K)
+        fit = {"kernel": "srt3d_fit_pixelwise", "iters": f.iters, "ms": fit_ms,
+               "pixel_iters_per_s": f.npix * f.iters / (fit_ms * 1e-3),
+               "roofline": roofline("srt3d_fit_pixelwise", f_b, f_f, fit_ms),
+               "note": "NEXT-2: the iterations of the step in one launch (no spatial regulariser between data "
+                       "steps); bitwise equal to iters x srt3d_sketch_grad_step; timed outside the step"}
     stream = None
     if stream_ms is not None:
         # bucketing: read each (uint32 pixel, uint16 bin) event once, write its bin, write offsets
@@ -485,7 +512,7 @@ def run_srt3d(args):
             "data": "synthetic (seeded Eq. (1) photon frames; stand-in for the paper's head/camouflage datasets)",
             "config": config_obj(f, args), "clocks": clocks, "e2e": e2e,
             "gpu_launches": pipe.launches_per_step * args.steps,
-            "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad, "init": init,
+            "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad, "fit": fit, "init": init,
             "stream": stream,
             "step_definition": "srt3d_sketch over the frame + iters x srt3d_sketch_grad_step (CUDA graphs)"}
     print(json.dumps(line), flush=True)
