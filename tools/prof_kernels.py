@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--n", type=int, default=1000000)
     ap.add_argument("--skip-sketch", action="store_true")
     ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--next", action="store_true", help="also launch the NEXT-2/3/4 kernels once")
     a = ap.parse_args()
     f = srt3d_inputs.make_frame(a.config, n_per_pixel=a.n if a.config == "C4" else None)
     bins = torch.from_numpy(f.bins).cuda()
@@ -37,6 +38,13 @@ def main():
                 p.srt3d_descent_update(t, al, gt, ga, f.sigma, f.T, f.m)
             else:
                 p.srt3d_sketch_grad_step(z, t, al, f.sigma, f.T, f.m)
+    if a.next and f.iters:
+        t, al = t0.clone(), a0.clone()
+        p.srt3d_fit_pixelwise(z, t, al, f.sigma, f.T, f.m, f.iters)
+        p.srt3d_init_depths(z, f.sigma, f.T, min(4096, 16 * f.m), f.K, 50)
+        p.srt3d_init_k1(z, f.sigma, f.T)
+        n = (offs[1:].to(torch.int64) - offs[:-1].to(torch.int64)).to(torch.int32).view(torch.uint32).contiguous()
+        p.srt3d_sketch_merge(z, n, z.clone(), n.clone())
     torch.cuda.synchronize()
     print("ok", f.name, f.n_photons)
 
