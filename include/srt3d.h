@@ -234,7 +234,8 @@ int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, con
 
 /*
  * srt3d_bucket_events — an unsorted stream of photon events (pixel index,
- * bin) into the pixel-sorted CSR frame srt3d_sketch consumes (reading A21):
+ * bin) into the pixel-sorted CSR frame srt3d_sketch consumes (reading A21),
+ * by a two-level counting sort with coalesced writes:
  * offsets[i] = number of events with pixel < i, offsets[npix] = kept events,
  * and each pixel's bins contiguous in bins_out.  Within a pixel the order
  * follows atomic arrival (a permutation of the stable order; the sketch is
@@ -243,11 +244,12 @@ int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, con
  *   pix uint32 [nevents], bins uint16 [nevents] (bins < T is the same
  *   precondition as for srt3d_sketch), nevents < 2^32; offsets uint32
  *   [npix+1] and bins_out uint16 [nevents] outputs; scratch uint32
- *   [srt3d_bucket_scratch_words(npix)] device workspace owned by the caller.
+ *   [srt3d_bucket_scratch_words(npix, nevents)] device workspace owned by the
+ *   caller (about nevents + 512 * nevents / 32768 words).
  */
 int srt3d_bucket_events(const uint32_t* pix, const uint16_t* bins, uint64_t nevents, int64_t npix,
                         uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch, uint32_t* dropped, void* stream);
-uint64_t srt3d_bucket_scratch_words(int64_t npix);
+uint64_t srt3d_bucket_scratch_words(int64_t npix, uint64_t nevents);
 
 /*
  * srt3d_check_csr — debug validator (not on the hot path).  Sets *bad (a

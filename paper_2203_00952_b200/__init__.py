@@ -77,7 +77,7 @@ def load_library(path: str | None = None):
     lib.srt3d_init_k1.argtypes = [P, i64, f32, u32, u32, P, P, P]
     lib.srt3d_sketch_merge.argtypes = [P, P, P, P, i64, u32, P, P, P]
     lib.srt3d_bucket_events.argtypes = [P, P, u64, i64, P, P, P, P, P]
-    lib.srt3d_bucket_scratch_words.argtypes = [i64]
+    lib.srt3d_bucket_scratch_words.argtypes = [i64, u64]
     lib.srt3d_bucket_scratch_words.restype = u64
     for f in EXPORTS[2:]:
         getattr(lib, f).restype = ctypes.c_int
@@ -237,9 +237,9 @@ def srt3d_sketch_merge(za, na, zb, nb, z_out=None, n_out=None, stream=None):
     return z_out, n_out
 
 
-def srt3d_bucket_scratch_words(npix: int) -> int:
-    """uint32 words of device workspace srt3d_bucket_events needs for npix pixels."""
-    return int(load_library().srt3d_bucket_scratch_words(int(npix)))
+def srt3d_bucket_scratch_words(npix: int, nevents: int) -> int:
+    """uint32 words of device workspace srt3d_bucket_events needs."""
+    return int(load_library().srt3d_bucket_scratch_words(int(npix), int(nevents)))
 
 
 def srt3d_bucket_events(pix, bins, npix: int, stream=None):
@@ -248,7 +248,7 @@ def srt3d_bucket_events(pix, bins, npix: int, stream=None):
     nev = pix.numel()
     offsets = torch.empty(npix + 1, dtype=torch.uint32, device=dev)
     out = torch.empty(max(nev, 1), dtype=torch.uint16, device=dev)
-    scratch = torch.empty(srt3d_bucket_scratch_words(npix), dtype=torch.uint32, device=dev)
+    scratch = torch.empty(max(1, srt3d_bucket_scratch_words(npix, nev)), dtype=torch.uint32, device=dev)
     dropped = torch.empty(1, dtype=torch.uint32, device=dev)
     _need_cuda(pix, bins)
     _call("srt3d_bucket_events", _ptr(pix), _ptr(bins), nev, int(npix), _ptr(offsets), _ptr(out), _ptr(scratch),

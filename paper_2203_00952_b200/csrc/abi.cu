@@ -386,8 +386,8 @@ int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, con
   return SRT3D_OK;
 }
 
-uint64_t srt3d_bucket_scratch_words(int64_t npix) {
-  return npix < 0 ? 0 : (uint64_t)srt3d::bucket_scratch_words(npix);
+uint64_t srt3d_bucket_scratch_words(int64_t npix, uint64_t nevents) {
+  return npix < 0 ? 0 : (uint64_t)srt3d::bucket_scratch_words(npix, nevents);
 }
 
 int srt3d_bucket_events(const uint32_t* pix, const uint16_t* bins, uint64_t nevents, int64_t npix,

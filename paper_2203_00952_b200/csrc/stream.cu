@@ -5,11 +5,23 @@
 //      — folds the sketch of a new photon batch into a running
 //     sketch; in place (z_out = z_a, n_out = n_a) is allowed.
 //   srt3d_bucket_events: an unsorted (pixel, bin) event stream -> the
-//     pixel-sorted CSR frame srt3d_sketch consumes (reading A21): count per
-//     pixel (global atomics), exclusive scan (block scan + scan of block sums
-//     + fix-up), scatter (atomic cursors).  The order of a pixel's bins follows
-//     atomic arrival, so the CSR is a valid permutation of the stable sort (the
-//     sketch is order-invariant up to fp32 rounding); offsets are exact.
+//     pixel-sorted CSR frame srt3d_sketch consumes (reading A21), as a
+//     two-level counting sort whose writes are coalesced:
+//       A. per chunk of 32768 events, a shared-memory histogram of the coarse
+//          key (pixel >> S, <= 512 buckets) -> table[bucket][chunk];
+//       scan of the table (bucket-major) -> the segment of every
+//          (bucket, chunk) in a packed temp buffer;
+//       B. the chunk again: each event to its segment through shared-memory
+//          cursors, packed as (pixel & (2^S - 1)) << 16 | bin;
+//       C. one CTA per bucket: histogram of the local pixel -> exact per-pixel
+//          offsets; then tiles of 4096 events are counting-sorted in shared
+//          memory and written out in pixel order (runs of consecutive
+//          addresses instead of one random 2-byte store per event).
+//     Within a pixel the order follows shared-memory atomic arrival (a valid
+//     permutation of the stable order; the sketch is order-invariant up to
+//     fp32 rounding); offsets are exact.  Frames with more than 512 * 8192
+//     pixels use a one-level variant (global atomic counts, scan, atomic
+//     scatter).
 #include <cstdint>
 
 #include "common.cuh"
@@ -54,9 +66,29 @@ constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_PER_THREAD = 4;
 constexpr long long SCAN_TILE = (long long)SCAN_THREADS * SCAN_PER_THREAD;
 
-size_t bucket_scratch_words(long long npix) {
-  const long long nb = (npix + SCAN_TILE - 1) / SCAN_TILE;
-  return (size_t)npix + (size_t)nb + 2;  // counts/cursors, block sums, dropped
+constexpr int BK_CHUNK = 32768;     // events per CTA in passes A and B
+constexpr int BK_MAX_BUCKETS = 512;  // coarse buckets
+constexpr int BK_MAX_S = 13;         // log2 pixels per bucket (local pixel id in 16 bits, smem histograms)
+constexpr int BK_TILE = 8192;        // events per shared-memory sorted tile (passes B, C)
+
+static int bucket_shift(long long npix) {
+  int S = 0;
+  while ((npix + (1ll << S) - 1) >> S > BK_MAX_BUCKETS) S++;
+  return S;
+}
+static bool bucket_two_level(long long npix) { return npix > 0 && bucket_shift(npix) <= BK_MAX_S; }
+
+size_t bucket_scratch_words(long long npix, unsigned long long nev) {
+  if (!bucket_two_level(npix)) {
+    const long long nb = (npix + SCAN_TILE - 1) / SCAN_TILE;
+    return (size_t)npix + (size_t)nb + 2;  // counts/cursors, block sums, dropped, total
+  }
+  const int S = bucket_shift(npix);
+  const long long NB = (npix + (1ll << S) - 1) >> S;
+  const long long nch = ((long long)nev + BK_CHUNK - 1) / BK_CHUNK;
+  const long long tn = NB * (nch > 0 ? nch : 1) + 1;
+  // temp, table (+ total), scan block sums, dropped, total
+  return (size_t)nev + (size_t)tn + (size_t)((tn + SCAN_TILE - 1) / SCAN_TILE) + 2;
 }
 
 __global__ void count_kernel(const uint32_t* __restrict__ pix, unsigned long long nev, long long npix,
@@ -201,14 +233,266 @@ __global__ void scatter_kernel(const uint32_t* __restrict__ pix, const uint16_t*
   }
 }
 
-cudaError_t launch_bucket(const uint32_t* pix, const uint16_t* bins, unsigned long long nev, long long npix,
-                          uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch, uint32_t* dropped_out,
-                          cudaStream_t s, int num_sms) {
+// ---- two-level bucketing ------------------------------------------------------
+// In-place exclusive scan helpers over n words: scan_tiles_kernel (block
+// prefix + block sums), scan_bsum_kernel, then add the block prefix.
+__global__ void scan_add_kernel(uint32_t* a, const uint32_t* bsum, long long n, const uint32_t* total) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride)
+    a[i] = i == n ? *total : a[i] + bsum[i / SCAN_TILE];
+}
+
+// Pass A: coarse histogram of one chunk -> table[b * nch + chunk].
+__global__ void __launch_bounds__(512) coarse_count_kernel(const uint32_t* __restrict__ pix, unsigned long long nev,
+                                                           long long npix, int S, int NB, long long nch,
+                                                           uint32_t* table, uint32_t* dropped) {
+  __shared__ uint32_t h[BK_MAX_BUCKETS];
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) h[b] = 0u;
+  __syncthreads();
+  const unsigned long long c0 = (unsigned long long)blockIdx.x * BK_CHUNK;
+  const unsigned long long c1 = min(nev, c0 + BK_CHUNK);
+  uint32_t drop = 0;
+  for (unsigned long long e0 = c0 + threadIdx.x; e0 < c1; e0 += 8 * blockDim.x) {  // 8 loads in flight
+    uint32_t p[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const unsigned long long e = e0 + q * blockDim.x;
+      p[q] = e < c1 ? __ldcs(pix + e) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if (e0 + q * blockDim.x >= c1) break;
+      if ((long long)p[q] < npix)
+        atomicAdd(&h[p[q] >> S], 1u);
+      else
+        drop++;
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) table[(long long)b * nch + blockIdx.x] = h[b];
+  if (drop) atomicAdd(dropped, drop);
+}
+
+// Pass B: the chunk again, in tiles of BK_TILE events counting-sorted by
+// bucket in shared memory, then written out in bucket order: consecutive
+// threads store consecutive addresses of a (bucket, chunk) segment.
+__device__ uint32_t block_scan_smem(uint32_t* a, int n, uint32_t* wsum);
+
+__global__ void __launch_bounds__(1024) partition_kernel(const uint32_t* __restrict__ pix,
+                                                         const uint16_t* __restrict__ bins, unsigned long long nev,
+                                                         long long npix, int S, int NB, long long nch,
+                                                         const uint32_t* table, uint32_t* temp) {
+  __shared__ uint32_t cur[BK_MAX_BUCKETS], tc[BK_MAX_BUCKETS], wsum[32];
+  extern __shared__ uint32_t pt_smem[];
+  uint32_t* sbuf = pt_smem;                                        // [BK_TILE] packed values
+  uint16_t* skey = reinterpret_cast<uint16_t*>(pt_smem + BK_TILE);  // [BK_TILE] bucket
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+    cur[b] = table[(long long)b * nch + blockIdx.x];
+    tc[b] = 0u;
+  }
+  __syncthreads();
+  const unsigned long long c0 = (unsigned long long)blockIdx.x * BK_CHUNK;
+  const unsigned long long c1 = min(nev, c0 + BK_CHUNK);
+  const uint32_t mask = (1u << S) - 1u;
+  constexpr int PER = BK_TILE / 1024;
+  for (unsigned long long t0 = c0; t0 < c1; t0 += BK_TILE) {
+    uint32_t key[PER], val[PER], rk[PER];
+#pragma unroll
+    for (int q = 0; q < PER; q++) {  // all loads of the tile in flight
+      const unsigned long long e = t0 + threadIdx.x + q * 1024;
+      const uint32_t p = e < c1 ? __ldcs(pix + e) : 0xffffffffu;
+      val[q] = e < c1 ? (uint32_t)__ldcs(bins + e) : 0u;
+      key[q] = (long long)p < npix ? (p >> S) : 0xffffffffu;
+      val[q] |= (p & mask) << 16;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; q++) rk[q] = key[q] != 0xffffffffu ? atomicAdd(&tc[key[q]], 1u) : 0u;
+    __syncthreads();
+    const uint32_t nt = block_scan_smem(tc, NB, wsum);  // tile offsets per bucket; kept events in the tile
+#pragma unroll
+    for (int q = 0; q < PER; q++)
+      if (key[q] != 0xffffffffu) {
+        sbuf[tc[key[q]] + rk[q]] = val[q];
+        skey[tc[key[q]] + rk[q]] = (uint16_t)key[q];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+      const uint32_t i = threadIdx.x + q * 1024;
+      if (i < nt) {
+        const uint32_t b = skey[i];
+        temp[cur[b] + i - tc[b]] = sbuf[i];
+      }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+      const uint32_t nxt = b + 1 < NB ? tc[b + 1] : nt;
+      cur[b] += nxt - tc[b];
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) tc[b] = 0u;
+    __syncthreads();
+  }
+}
+
+// Exclusive block scan of n <= 8192 shared words (in place); returns the total.
+__device__ uint32_t block_scan_smem(uint32_t* a, int n, uint32_t* wsum) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;  // contiguous run per thread
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  uint32_t t = 0;
+  for (int i = lo; i < hi; i++) t += a[i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = t;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t w = lane < nw ? wsum[lane] : 0u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < nw) wsum[lane] = w;
+  }
+  __syncthreads();
+  uint32_t run = x - t + (warp ? wsum[warp - 1] : 0u);
+  const uint32_t total = wsum[(blockDim.x >> 5) - 1];
+  for (int i = lo; i < hi; i++) {
+    const uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  return total;
+}
+
+// Pass C: one CTA per bucket — per-pixel offsets, then tile-sorted coalesced output.
+__global__ void __launch_bounds__(1024) bucket_fine_kernel(const uint32_t* __restrict__ temp, const uint32_t* table,
+                                                          long long npix, int S, long long nch, int NB,
+                                                          uint32_t* offsets, uint16_t* out) {
+  extern __shared__ uint32_t bk_smem[];
+  const int P = 1 << S;
+  uint32_t* cur = bk_smem;           // [P] global cursor of each local pixel
+  uint32_t* tc = cur + P;            // [P] tile counts -> tile offsets
+  uint32_t* sbuf = tc + P;           // [BK_TILE] tile sorted
+  __shared__ uint32_t wsum[32];
+  const int b = blockIdx.x;
+  const uint32_t bs = table[(long long)b * nch], be = table[(long long)(b + 1) * nch];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    cur[i] = 0u;
+    tc[i] = 0u;
+  }
+  __syncthreads();
+  for (uint32_t i0 = bs + threadIdx.x; i0 < be; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t i = i0 + q * blockDim.x;
+      w[q] = i < be ? __ldcg(temp + i) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      if (w[q] != 0xffffffffu) atomicAdd(&cur[w[q] >> 16], 1u);
+  }
+  __syncthreads();
+  block_scan_smem(cur, P, wsum);
+  const long long p0 = (long long)b << S;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    cur[i] += bs;
+    if (p0 + i < npix) offsets[p0 + i] = cur[i];
+  }
+  if (b == NB - 1 && threadIdx.x == 0) offsets[npix] = be;
+  __syncthreads();
+  for (uint32_t t0 = bs; t0 < be; t0 += BK_TILE) {
+    const int nt = (int)min((uint32_t)BK_TILE, be - t0);
+    uint32_t v[BK_TILE / 1024], r[BK_TILE / 1024];
+#pragma unroll
+    for (int q = 0; q < BK_TILE / 1024; q++) {
+      const int i = threadIdx.x + q * 1024;
+      v[q] = i < nt ? temp[t0 + i] : 0u;
+      r[q] = i < nt ? atomicAdd(&tc[v[q] >> 16], 1u) : 0u;
+    }
+    __syncthreads();
+    block_scan_smem(tc, P, wsum);  // tc: tile offsets of every local pixel
+#pragma unroll
+    for (int q = 0; q < BK_TILE / 1024; q++) {
+      const int i = threadIdx.x + q * 1024;
+      if (i < nt) sbuf[tc[v[q] >> 16] + r[q]] = v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BK_TILE / 1024; q++) {
+      const int i = threadIdx.x + q * 1024;
+      if (i < nt) {
+        const uint32_t w = sbuf[i];
+        const uint32_t lp = w >> 16;
+        out[cur[lp] + (uint32_t)i - tc[lp]] = (uint16_t)(w & 0xffffu);  // consecutive i, same pixel: consecutive addresses
+      }
+    }
+    __syncthreads();
+    // advance the cursors by this tile's counts (tc holds offsets: count = next offset - offset)
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      const uint32_t nxt = i + 1 < P ? tc[i + 1] : (uint32_t)nt;
+      r[0] = nxt - tc[i];
+      cur[i] += r[0];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x) tc[i] = 0u;
+    __syncthreads();
+  }
+}
+
+static cudaError_t launch_bucket_two_level(const uint32_t* pix, const uint16_t* bins, unsigned long long nev,
+                                          long long npix, uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch,
+                                          uint32_t* dropped_out, cudaStream_t s, int num_sms) {
+  const int S = bucket_shift(npix);
+  const int NB = (int)((npix + (1ll << S) - 1) >> S);
+  const long long nch = ((long long)nev + BK_CHUNK - 1) / BK_CHUNK;
+  const long long nchv = nch > 0 ? nch : 1;
+  const long long tn = (long long)NB * nchv;
+  uint32_t* temp = scratch;
+  uint32_t* table = temp + nev;             // [tn + 1]
+  uint32_t* bsum = table + tn + 1;          // [ceil((tn+1) / SCAN_TILE)]
+  const long long nbs = (tn + 1 + SCAN_TILE - 1) / SCAN_TILE;
+  uint32_t* misc = bsum + nbs;              // [0] dropped, [1] total
+  cudaError_t e = cudaMemsetAsync(table, 0, sizeof(uint32_t) * (size_t)(tn + 1 + nbs + 2), s);
+  if (e != cudaSuccess) return e;
+  if (nch > 0) coarse_count_kernel<<<(unsigned)nch, 512, 0, s>>>(pix, nev, npix, S, NB, nch, table, misc);
+  scan_tiles_kernel<<<(unsigned)((tn + SCAN_TILE - 1) / SCAN_TILE), SCAN_THREADS, 0, s>>>(table, tn, table, bsum);
+  scan_bsum_kernel<<<1, SCAN_THREADS, 0, s>>>(bsum, (tn + SCAN_TILE - 1) / SCAN_TILE, misc + 1);
+  long long fg = (tn + 1 + 255) / 256;
+  if (fg > (long long)num_sms * 16) fg = (long long)num_sms * 16;
+  scan_add_kernel<<<(unsigned)fg, 256, 0, s>>>(table, bsum, tn, misc + 1);
+  const size_t psmem = sizeof(uint32_t) * BK_TILE + sizeof(uint16_t) * BK_TILE;
+  e = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+  if (e != cudaSuccess) return e;
+  if (nch > 0) partition_kernel<<<(unsigned)nch, 1024, psmem, s>>>(pix, bins, nev, npix, S, NB, nch, table, temp);
+  // with no events the table is all zeros: pass C writes zero offsets
+  const size_t smem = sizeof(uint32_t) * ((size_t)2 * (1u << S) + BK_TILE);
+  e = cudaFuncSetAttribute(bucket_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  bucket_fine_kernel<<<(unsigned)NB, 1024, smem, s>>>(temp, table, npix, S, nchv, NB, offsets, bins_out);
+  if (dropped_out) {
+    e = cudaMemcpyAsync(dropped_out, misc, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_bucket_atomic(const uint32_t* pix, const uint16_t* bins, unsigned long long nev,
+                                        long long npix, uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch,
+                                        uint32_t* dropped_out, cudaStream_t s, int num_sms) {
   const long long nb = (npix + SCAN_TILE - 1) / SCAN_TILE;
   uint32_t* cnt = scratch;            // [npix]: counts, then cursors
   uint32_t* bsum = scratch + npix;    // [nb]
   uint32_t* misc = bsum + nb;         // [0] dropped, [1] total
-  cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * bucket_scratch_words(npix), s);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * ((size_t)npix + (size_t)nb + 2), s);
   if (e != cudaSuccess) return e;
   const long long ev_grid = (long long)num_sms * 8;
   if (nev) count_kernel<<<(unsigned)ev_grid, 256, 0, s>>>(pix, nev, npix, cnt, misc);
@@ -225,6 +509,14 @@ cudaError_t launch_bucket(const uint32_t* pix, const uint16_t* bins, unsigned lo
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_bucket(const uint32_t* pix, const uint16_t* bins, unsigned long long nev, long long npix,
+                          uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch, uint32_t* dropped_out,
+                          cudaStream_t s, int num_sms) {
+  if (bucket_two_level(npix))
+    return launch_bucket_two_level(pix, bins, nev, npix, offsets, bins_out, scratch, dropped_out, s, num_sms);
+  return launch_bucket_atomic(pix, bins, nev, npix, offsets, bins_out, scratch, dropped_out, s, num_sms);
 }
 
 }  // namespace srt3d

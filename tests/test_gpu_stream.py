@@ -34,7 +34,9 @@ def _events(npix, T, n_ev, seed, extra_bad=0):
 
 
 @pytest.mark.parametrize("npix,T,n_ev,bad", [(1000, 4096, 200000, 0), (262144, 8192, 1000000, 17),
-                                             (5000, 1024, 0, 0), (1, 100, 5000, 3), (70000, 2500, 300000, 0)])
+                                             (5000, 1024, 0, 0), (1, 100, 5000, 3), (70000, 2500, 300000, 0),
+                                             (513, 4096, 40000, 5), (4194304, 1024, 300000, 0),
+                                             (5000000, 2048, 200000, 2)])
 def test_bucket_events_parity(gpu, oracle_mod, npix, T, n_ev, bad):
     import torch
 
@@ -116,4 +118,4 @@ def test_stream_errors(gpu):
     z65 = torch.zeros((4, 65), dtype=torch.complex64, device="cuda")
     with pytest.raises(gpu.Srt3dError):
         gpu.srt3d_sketch_merge(z65, n, z65, n)  # m > SRT3D_MAX_M
-    assert gpu.srt3d_bucket_scratch_words(262144) >= 262144
+    assert gpu.srt3d_bucket_scratch_words(262144, 1000) >= 1000
