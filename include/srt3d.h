@@ -233,6 +233,15 @@ int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, con
                        uint32_t m, float* z_out, uint32_t* n_out, void* stream);
 
 /*
+ * srt3d_sketch_accumulate — srt3d_sketch_merge in place into a running
+ * (z, n) with the batch counts taken from the batch's CSR offsets,
+ * n_b[i] = offsets_b[i+1] - offsets_b[i] (the offsets srt3d_sketch consumed to
+ * produce z_b): the online update of PAPER.md:65 for one batch.
+ */
+int srt3d_sketch_accumulate(float* z, uint32_t* n, const float* zb, const uint32_t* offsets_b, int64_t npix,
+                            uint32_t m, void* stream);
+
+/*
  * srt3d_bucket_events — an unsorted stream of photon events (pixel index,
  * bin) into the pixel-sorted CSR frame srt3d_sketch consumes (reading A21),
  * by a two-level counting sort with coalesced writes:

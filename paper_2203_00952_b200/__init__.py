@@ -38,7 +38,7 @@ EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
            "srt3d_sketch_plan", "srt3d_fit_pixelwise",
            "srt3d_backproject", "srt3d_init_depths", "srt3d_init_k1", "srt3d_sketch_merge",
-           "srt3d_bucket_events", "srt3d_bucket_scratch_words")
+           "srt3d_bucket_events", "srt3d_bucket_scratch_words", "srt3d_sketch_accumulate")
 
 
 class Srt3dError(RuntimeError):
@@ -77,6 +77,7 @@ def load_library(path: str | None = None):
     lib.srt3d_init_k1.argtypes = [P, i64, f32, u32, u32, P, P, P]
     lib.srt3d_sketch_merge.argtypes = [P, P, P, P, i64, u32, P, P, P]
     lib.srt3d_bucket_events.argtypes = [P, P, u64, i64, P, P, P, P, P]
+    lib.srt3d_sketch_accumulate.argtypes = [P, P, P, P, i64, u32, P]
     lib.srt3d_bucket_scratch_words.argtypes = [i64, u64]
     lib.srt3d_bucket_scratch_words.restype = u64
     for f in EXPORTS[2:]:
@@ -237,19 +238,31 @@ def srt3d_sketch_merge(za, na, zb, nb, z_out=None, n_out=None, stream=None):
     return z_out, n_out
 
 
+def srt3d_sketch_accumulate(z, n, zb, offsets_b, stream=None):
+    """NEXT-4: fold a batch sketch z_b (counts from its CSR offsets) into the running (z, n), in place."""
+    npix, m = z.shape
+    _need_cuda(z, n, zb, offsets_b)
+    _call("srt3d_sketch_accumulate", _ptr(z), _ptr(n), _ptr(zb), _ptr(offsets_b), npix, m, _stream(stream))
+    return z, n
+
+
 def srt3d_bucket_scratch_words(npix: int, nevents: int) -> int:
     """uint32 words of device workspace srt3d_bucket_events needs."""
     return int(load_library().srt3d_bucket_scratch_words(int(npix), int(nevents)))
 
 
-def srt3d_bucket_events(pix, bins, npix: int, stream=None):
-    """NEXT-4: unsorted (pixel uint32, bin uint16) events -> CSR (offsets uint32, bins uint16, dropped)."""
+def srt3d_bucket_events(pix, bins, npix: int, offsets=None, out=None, scratch=None, dropped=None, stream=None):
+    """NEXT-4: unsorted (pixel uint32, bin uint16) events -> CSR (offsets uint32, bins uint16, dropped).
+    Output / workspace tensors may be passed in (reused across batches)."""
     dev = pix.device
     nev = pix.numel()
-    offsets = torch.empty(npix + 1, dtype=torch.uint32, device=dev)
-    out = torch.empty(max(nev, 1), dtype=torch.uint16, device=dev)
-    scratch = torch.empty(max(1, srt3d_bucket_scratch_words(npix, nev)), dtype=torch.uint32, device=dev)
-    dropped = torch.empty(1, dtype=torch.uint32, device=dev)
+    offsets = torch.empty(npix + 1, dtype=torch.uint32, device=dev) if offsets is None else offsets
+    out = torch.empty(max(nev, 1), dtype=torch.uint16, device=dev) if out is None else out
+    if scratch is None:
+        scratch = torch.empty(max(1, srt3d_bucket_scratch_words(npix, nev)), dtype=torch.uint32, device=dev)
+    dropped = torch.empty(1, dtype=torch.uint32, device=dev) if dropped is None else dropped
+    if out.numel() < nev or scratch.numel() < srt3d_bucket_scratch_words(npix, nev) or offsets.numel() != npix + 1:
+        raise ValueError("bucket_events: output / scratch tensors too small")
     _need_cuda(pix, bins)
     _call("srt3d_bucket_events", _ptr(pix), _ptr(bins), nev, int(npix), _ptr(offsets), _ptr(out), _ptr(scratch),
           _ptr(dropped), _stream(stream))

@@ -380,9 +380,24 @@ int srt3d_sketch_merge(const float* za, const uint32_t* na, const float* zb, con
   if (!aligned(za, 8) || !aligned(zb, 8) || !aligned(z_out, 8) || !aligned(na, 4) || !aligned(nb, 4) ||
       !aligned(n_out, 4))
     return fail(SRT3D_EALIGN, "z must be 8-byte and n 4-byte aligned");
-  cudaError_t e = srt3d::launch_merge(za, na, zb, nb, npix, m, z_out, n_out, (cudaStream_t)stream,
+  cudaError_t e = srt3d::launch_merge(za, na, zb, nb, nullptr, npix, m, z_out, n_out, (cudaStream_t)stream,
                                       num_sms_current());
   if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch_merge");
+  return SRT3D_OK;
+}
+
+int srt3d_sketch_accumulate(float* z, uint32_t* n, const float* zb, const uint32_t* offsets_b, int64_t npix,
+                            uint32_t m, void* stream) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  if (m < 1) return fail(SRT3D_EINVAL, "m=%u < 1", m);
+  if (m > SRT3D_MAX_M) return fail(SRT3D_EUNSUPPORTED, "m=%u exceeds SRT3D_MAX_M=%u", m, SRT3D_MAX_M);
+  if (npix == 0) return SRT3D_OK;
+  if (!z || !n || !zb || !offsets_b) return fail(SRT3D_ENULL, "all pointers must be non-NULL");
+  if (!aligned(z, 8) || !aligned(zb, 8) || !aligned(n, 4) || !aligned(offsets_b, 4))
+    return fail(SRT3D_EALIGN, "z must be 8-byte and n/offsets 4-byte aligned");
+  cudaError_t e = srt3d::launch_merge(z, n, zb, nullptr, offsets_b, npix, m, z, n, (cudaStream_t)stream,
+                                      num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch_accumulate");
   return SRT3D_OK;
 }
 

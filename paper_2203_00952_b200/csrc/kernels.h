@@ -89,8 +89,9 @@ cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int n
 cudaError_t launch_init_k1(const BpArgs& a, cudaStream_t s);
 size_t backproject_smem(uint32_t N, bool pick);
 // NEXT-4 streaming acquisition (stream.cu).
-cudaError_t launch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb, long long npix,
-                         uint32_t m, float* zo, uint32_t* no, cudaStream_t s, int num_sms);
+cudaError_t launch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb,
+                         const uint32_t* offs_b, long long npix, uint32_t m, float* zo, uint32_t* no, cudaStream_t s,
+                         int num_sms);
 size_t bucket_scratch_words(long long npix, unsigned long long nev);
 cudaError_t launch_bucket(const uint32_t* pix, const uint16_t* bins, unsigned long long nev, long long npix,
                           uint32_t* offsets, uint16_t* bins_out, uint32_t* scratch, uint32_t* dropped_out,

@@ -31,13 +31,16 @@ namespace srt3d {
 
 // One warp per pixel: counts are read before the (possibly aliased) count
 // output is written; the row's m complex values are spread over the lanes.
+// nb == nullptr: n_b[i] = offs_b[i+1] - offs_b[i] (the batch's CSR offsets).
 __global__ void __launch_bounds__(256) merge_kernel(const float2* __restrict__ za, const uint32_t* na,
                                                     const float2* __restrict__ zb, const uint32_t* nb,
-                                                    long long npix, uint32_t m, float2* zo, uint32_t* no) {
+                                                    const uint32_t* offs_b, long long npix, uint32_t m, float2* zo,
+                                                    uint32_t* no) {
   const int lane = threadIdx.x & 31;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < npix; i += nw) {
-    const uint32_t a = na[i], b = nb[i];
+    const uint32_t a = na[i];
+    const uint32_t b = nb ? nb[i] : offs_b[i + 1] - offs_b[i];
     const uint64_t n = (uint64_t)a + b;
     const double inv = n ? 1.0 / (double)n : 0.0;
     const float wa = (float)((double)a * inv), wb = (float)((double)b * inv);
@@ -50,13 +53,14 @@ __global__ void __launch_bounds__(256) merge_kernel(const float2* __restrict__ z
   }
 }
 
-cudaError_t launch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb, long long npix,
-                         uint32_t m, float* zo, uint32_t* no, cudaStream_t s, int num_sms) {
+cudaError_t launch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb,
+                         const uint32_t* offs_b, long long npix, uint32_t m, float* zo, uint32_t* no, cudaStream_t s,
+                         int num_sms) {
   if (npix <= 0) return cudaSuccess;
   long long grid = (npix + 7) / 8;
   if (grid > (long long)num_sms * 16) grid = (long long)num_sms * 16;
   merge_kernel<<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const float2*>(za), na,
-                                              reinterpret_cast<const float2*>(zb), nb, npix, m,
+                                              reinterpret_cast<const float2*>(zb), nb, offs_b, npix, m,
                                               reinterpret_cast<float2*>(zo), no);
   return cudaGetLastError();
 }

@@ -119,3 +119,38 @@ def test_stream_errors(gpu):
     with pytest.raises(gpu.Srt3dError):
         gpu.srt3d_sketch_merge(z65, n, z65, n)  # m > SRT3D_MAX_M
     assert gpu.srt3d_bucket_scratch_words(262144, 1000) >= 1000
+
+
+@pytest.mark.parametrize("T,m", [(4096, 10), (8192, 32)])
+def test_streaming_sketcher_equals_batch_sketch(gpu, oracle_mod, T, m):
+    """PAPER.md:65 online acquisition: three event batches folded by StreamingSketcher
+    (bucket -> sketch -> accumulate) equal the sketch of all kept events at once; counts exact;
+    out-of-range pixels dropped and counted; srt3d_sketch_accumulate == srt3d_sketch_merge."""
+    import torch
+
+    from paper_2203_00952_b200.stream import StreamingSketcher
+
+    npix = 2000
+    batches = [_events(npix, T, n, seed=T + n, extra_bad=b) for n, b in ((100000, 0), (37000, 4), (120000, 0))]
+    st = StreamingSketcher(npix, T, m, max_batch=120000)
+    for p, b in batches:
+        st.add(_dev(p), _dev(b))
+    torch.cuda.synchronize()
+    p_all = np.concatenate([p for p, _ in batches])
+    b_all = np.concatenate([b for _, b in batches])
+    oo, ob, od = oracle_mod.bucket_events(p_all, b_all, npix)
+    zo = oracle_mod.sketch(ob, oo, T, m)
+    zg = st.z.cpu().numpy()
+    assert max(np.abs(zg.real - zo.real).max(), np.abs(zg.imag - zo.imag).max()) <= 1e-5
+    assert np.array_equal(st.n.cpu().numpy(), np.diff(oo.astype(np.int64)).astype(np.uint32))
+    assert int(st.dropped_total.item()) == od == 4
+    # accumulate == merge with explicit counts
+    offs, out, _ = gpu.srt3d_bucket_events(_dev(batches[0][0]), _dev(batches[0][1]), npix)
+    zb = gpu.srt3d_sketch(out, offs, T, m, total_photons=100000)
+    za, na = st.z.clone(), st.n.clone()
+    nb = torch.from_numpy(np.diff(offs.cpu().numpy().astype(np.int64)).astype(np.uint32)).cuda()
+    zm, nm = gpu.srt3d_sketch_merge(za, na, zb, nb)
+    gpu.srt3d_sketch_accumulate(za, na, zb, offs)
+    torch.cuda.synchronize()
+    assert np.array_equal(za.cpu().numpy().view(np.uint64), zm.cpu().numpy().view(np.uint64))
+    assert np.array_equal(na.cpu().numpy(), nm.cpu().numpy())
