@@ -21,6 +21,9 @@
 // expected-sketch output goes the same way in reverse.  (Reading z row-wise
 // straight from global memory touches 32 sectors per warp load — L1-wavefront
 // bound; a register-staged copy serialises load -> store.)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -84,6 +87,31 @@ __device__ __forceinline__ void warp_slab_store(const float2* tile, float2* gdst
   }
 }
 
+// ---- TMA staging of the z slab (m % 16 == 0) ----------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)  // suspend-time hint (ns)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // The harness update (reading A13) for one (pixel, k); shared by the fused
 // step and K4 so both produce bit-identical results.
 __device__ __forceinline__ void update_one(const PixArgs& a, float tk, float ak, float gt, float ga, float& tn,
@@ -116,10 +144,10 @@ __device__ __forceinline__ void load_theta(const PixArgs& a, long long i, float 
 // Evaluates one pixel: Phi (PX_EXPECTED: written to zrow), else the loss L and
 // the gradient (gt, ga).  WAIT_Z: wait for the warp's cp.async z slab after
 // the anchors (which overlap the copy).
-template <int K, int M, int MODE, bool WAIT_Z = true>
+template <int K, int M, int MODE, bool WAIT_Z = true, bool ZTMA = false>
 __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const float* s_hh, const float* s_wh,
                                            const float (&tk)[K], const float (&ak)[K], float (&gt)[K],
-                                           float (&ga)[K], float& L) {
+                                           float (&ga)[K], float& L, uint64_t* zbar = nullptr) {
   const int m = M ? M : (int)a.m;
   uint32_t q[K];
   u64 W[K], Wn[K], P[K];
@@ -133,9 +161,13 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
   }
 
   if (MODE != PX_EXPECTED && WAIT_Z) {
-    // the anchors above overlap the z slab's cp.async; wait for it only now
-    cp_async_wait_all();
-    __syncwarp();
+    // the anchors above overlap the z slab's copy; wait for it only now
+    if (ZTMA) {
+      mbar_wait(zbar, 0);
+    } else {
+      cp_async_wait_all();
+      __syncwarp();
+    }
   }
   u64 L2 = 0ull;  // packed (sum r_r^2, sum r_i^2)
   u64 GA[K], GT[K];  // packed partial sums: GA = sum (rho_r p_r, rho_i p_i); GT = sum (s_r p_i, -s_i p_r)
@@ -170,7 +202,12 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
     }
     const float wh = M ? a.c.wh[j] : s_wh[j];
     float2 zj;
-    if (M > 0 && (M & 1) == 0) {  // LDS.128: z_j, z_{j+1} (conflict-free with S = m + 2)
+    if (ZTMA) {  // TMA box h = j / 16 (4 KB, 32 rows x 128 B, 128B swizzle): chunk (j%16)/2 ^ (row & 7)
+      const int r7 = (threadIdx.x & 7) << 4;
+      const float4 z2 = *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(zrow) + (j / 16) * 4096 +
+                                                         ((((j % 16) / 2) << 4) ^ r7));
+      zj = (j & 1) ? make_float2(z2.z, z2.w) : make_float2(z2.x, z2.y);
+    } else if (M > 0 && (M & 1) == 0) {  // LDS.128: z_j, z_{j+1} (conflict-free with S = m + 2)
       const float4 z2 = *reinterpret_cast<const float4*>(zrow + (j & ~1));
       zj = (j & 1) ? make_float2(z2.z, z2.w) : make_float2(z2.x, z2.y);
     } else {
@@ -278,6 +315,56 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_MIN_BLOCKS) grad_kernel(con
   float gt[K], ga[K], L;
   pixel_body<K, M, MODE>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
   if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
+}
+
+// Gradient / fused step for m % 16 == 0: the warp's 32 z rows arrive by TMA —
+// m/16 boxes of 32 rows x 32 floats (128 B) with the 128-byte swizzle, one
+// instruction each from one lane, completing on the warp's mbarrier — instead
+// of m/2 cp.async per lane plus their address arithmetic.  The swizzle places
+// 16-byte chunk c of row r at chunk c ^ (r & 7), so the per-thread LDS.128 row
+// reads of a quarter-warp hit 8 different bank groups (conflict-free) with no
+// padding.  Rows past the frame end are zero-filled by the TMA unit.
+template <int K, int M, int MODE>
+__global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel_tma(const PixArgs a,
+                                                                                const __grid_constant__ CUtensorMap tm) {
+  static_assert(M > 0 && M % 16 == 0, "TMA boxes of 32 floats");
+  constexpr int NBOX = M / 16;
+  extern __shared__ unsigned char tma_smem_raw[];
+  unsigned char* smem = tma_smem_raw + ((1024u - (smem_u32(tma_smem_raw) & 1023u)) & 1023u);  // 1 KB aligned
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
+  if (row0 >= a.npix) return;
+  unsigned char* tile = smem + (size_t)warp * NBOX * 4096;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(GRAD_THREADS / 32) * NBOX * 4096) + warp;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, NBOX * 4096u);
+#pragma unroll
+    for (int h = 0; h < NBOX; h++) tma_load_2d(tile + h * 4096, &tm, h * 32, (int)row0, bar);
+  }
+  __syncwarp();
+  const long long i = row0 + lane;
+  const bool active = i < a.npix;
+  float tk[K], ak[K];
+  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
+  float gt[K], ga[K], L;
+  pixel_body<K, M, MODE, true, true>(a, reinterpret_cast<float2*>(tile + lane * 128), nullptr, nullptr, tk, ak, gt,
+                                     ga, L, bar);
+  if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (static cudart).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
 }
 
 // NEXT-2: `iters` fused data steps per pixel in one launch.
@@ -437,6 +524,32 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
   const int gwarps = GRAD_THREADS / 32;
   const size_t smem = sizeof(float2) * gwarps * 32 * S;
   const int smem_max = (int)(sizeof(float2) * gwarps * 32 * zstride(MAX_M));
+  if constexpr (M > 0 && M % 16 == 0) {
+    if (((uintptr_t)a.z & 15u) == 0 && a.npix < (1ll << 31)) {
+      PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+      if (enc) {
+        CUtensorMap tm;
+        const cuuint64_t gdim[2] = {(cuuint64_t)(2 * M), (cuuint64_t)a.npix};
+        const cuuint64_t gstride[1] = {(cuuint64_t)(2 * M * sizeof(float))};
+        const cuuint32_t box[2] = {32u, 32u}, estride[2] = {1u, 1u};
+        if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.z), gdim, gstride, box, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+          auto tfn = grad_kernel_tma<K, M, MODE>;
+          const size_t tsmem = 1024 + (size_t)gwarps * (M / 16) * 4096 + 8 * gwarps;
+          static bool tattr = false;
+          if (!tattr) {
+            cudaError_t e = cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+            if (e != cudaSuccess) return e;
+            tattr = true;
+          }
+          const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
+          tfn<<<(unsigned)grid, GRAD_THREADS, tsmem, s>>>(a, tm);
+          return cudaGetLastError();
+        }
+      }
+    }
+  }
   auto fn = grad_kernel<K, M, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
