@@ -163,7 +163,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
   if (MODE != PX_EXPECTED && WAIT_Z) {
     // the anchors above overlap the z slab's copy; wait for it only now
     if (ZTMA) {
-      mbar_wait(zbar, 0);
+      mbar_wait(zbar, 0);  // box 0 (j < 16); later boxes are awaited inside the j loop
     } else {
       cp_async_wait_all();
       __syncwarp();
@@ -179,6 +179,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
 
 #pragma unroll(M ? M : 1)
   for (int j = 0; j < m; j++) {  // frequency j+1
+    if (ZTMA && MODE != PX_EXPECTED && WAIT_Z && j > 0 && j % 16 == 0) mbar_wait(zbar + j / 16, 0);
     if (j > 0) {
       if ((j & 31) == 0) {
 #pragma unroll
@@ -335,13 +336,18 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
   const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
   if (row0 >= a.npix) return;
   unsigned char* tile = smem + (size_t)warp * NBOX * 4096;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(GRAD_THREADS / 32) * NBOX * 4096) + warp;
+  // one mbarrier per box: the j loop waits for box h only when it reaches j = 16 h,
+  // so later boxes land while the first frequencies are computed
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(GRAD_THREADS / 32) * NBOX * 4096) + warp * NBOX;
   if (lane == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar, NBOX * 4096u);
 #pragma unroll
-    for (int h = 0; h < NBOX; h++) tma_load_2d(tile + h * 4096, &tm, h * 32, (int)row0, bar);
+    for (int h = 0; h < NBOX; h++) mbar_init(bar + h, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int h = 0; h < NBOX; h++) {
+      mbar_expect_tx(bar + h, 4096u);
+      tma_load_2d(tile + h * 4096, &tm, h * 32, (int)row0, bar + h);
+    }
   }
   __syncwarp();
   const long long i = row0 + lane;
@@ -536,7 +542,7 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
           auto tfn = grad_kernel_tma<K, M, MODE>;
-          const size_t tsmem = 1024 + (size_t)gwarps * (M / 16) * 4096 + 8 * gwarps;
+          const size_t tsmem = 1024 + (size_t)gwarps * (M / 16) * (4096 + 8);
           static bool tattr = false;
           if (!tattr) {
             cudaError_t e = cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
