@@ -425,12 +425,18 @@ def run_srt3d(args):
     sk_bytes = 2.0 * f.n_photons + 4.0 * (f.npix + 1) + 8.0 * f.m * f.npix
     direct_sum = path in (srt3d.PATH_DIRECT, srt3d.PATH_PAIRED)
     sk_flops = 8.0 * f.m * (f.n_photons if direct_sum else f.T * f.npix)
+    try:
+        fp32_meas = srt3d.srt3d_debug_ffma_peak() * 1e12  # K8, measured in this run
+    except Exception:  # pragma: no cover - measurement utility only
+        fp32_meas = None
     sketch = {"kernel": "srt3d_sketch",
               "path": {srt3d.PATH_DIRECT: "direct", srt3d.PATH_PAIRED: "paired"}.get(path, "bincount"),
               "lanes_per_pixel": lanes, "ms": sk_avg, "photons_per_s": f.n_photons / (sk_avg * 1e-3),
               "gbs": sk_bytes / (sk_avg * 1e-3) / 1e9, "frac_hbm": (sk_bytes / (sk_avg * 1e-3) / 1e9) / hbm,
               "tflops_direct_count": 8.0 * f.m * f.n_photons / (sk_avg * 1e-3) / 1e12,
-              "roofline": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_avg)}
+              "roofline": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_avg),
+              "fp32_measured_tflops": fp32_meas / 1e12 if fp32_meas else None,
+              "frac_of_measured_fp32": (sk_flops / (sk_avg * 1e-3)) / fp32_meas if fp32_meas else None}
     grad = None
     if f.iters > 0:
         per_iter = it_avg / f.iters

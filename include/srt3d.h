@@ -269,6 +269,16 @@ int srt3d_check_csr(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
                     void* stream);
 
 /*
+ * srt3d_debug_ffma_peak — measurement utility: the FP32
+ * FMA throughput the current device sustains now, in TFLOP/s (2 flops per
+ * FMA lane-op; 8 independent FFMA chains per thread on every SM, timed with
+ * CUDA events on the legacy stream; synchronous; allocates 4 bytes).  The
+ * bench reports the sketch's FP32 roofline against this and against the
+ * unit-count peak.  Not part of the method.
+ */
+int srt3d_debug_ffma_peak(double* tflops);
+
+/*
  * srt3d_debug_phase_index — test export of the exact integer phase index
  * used by srt3d_sketch: r[p][j-1] = (j * bins[p]) mod T, j = 1..m, computed
  * by the same device function the sketch kernel uses (PAPER.md:61 with

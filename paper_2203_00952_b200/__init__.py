@@ -38,7 +38,7 @@ EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
            "srt3d_sketch_plan", "srt3d_fit_pixelwise",
            "srt3d_backproject", "srt3d_init_depths", "srt3d_init_k1", "srt3d_sketch_merge",
-           "srt3d_bucket_events", "srt3d_bucket_scratch_words", "srt3d_sketch_accumulate")
+           "srt3d_bucket_events", "srt3d_bucket_scratch_words", "srt3d_sketch_accumulate", "srt3d_debug_ffma_peak")
 
 
 class Srt3dError(RuntimeError):
@@ -78,6 +78,7 @@ def load_library(path: str | None = None):
     lib.srt3d_sketch_merge.argtypes = [P, P, P, P, i64, u32, P, P, P]
     lib.srt3d_bucket_events.argtypes = [P, P, u64, i64, P, P, P, P, P]
     lib.srt3d_sketch_accumulate.argtypes = [P, P, P, P, i64, u32, P]
+    lib.srt3d_debug_ffma_peak.argtypes = [P]
     lib.srt3d_bucket_scratch_words.argtypes = [i64, u64]
     lib.srt3d_bucket_scratch_words.restype = u64
     for f in EXPORTS[2:]:
@@ -244,6 +245,13 @@ def srt3d_sketch_accumulate(z, n, zb, offsets_b, stream=None):
     _need_cuda(z, n, zb, offsets_b)
     _call("srt3d_sketch_accumulate", _ptr(z), _ptr(n), _ptr(zb), _ptr(offsets_b), npix, m, _stream(stream))
     return z, n
+
+
+def srt3d_debug_ffma_peak() -> float:
+    """Measured FP32 FMA throughput of the current device now (TFLOP/s)."""
+    v = ctypes.c_double(0.0)
+    _call("srt3d_debug_ffma_peak", ctypes.byref(v))
+    return float(v.value)
 
 
 def srt3d_bucket_scratch_words(npix: int, nevents: int) -> int:

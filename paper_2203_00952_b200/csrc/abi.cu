@@ -431,6 +431,13 @@ int srt3d_check_csr(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   return SRT3D_OK;
 }
 
+int srt3d_debug_ffma_peak(double* tflops) {
+  if (!tflops) return fail(SRT3D_ENULL, "tflops must be non-NULL");
+  cudaError_t e = srt3d::measure_ffma_peak(tflops, num_sms_current());
+  if (e != cudaSuccess) return cuda_fail(e, "srt3d_debug_ffma_peak");
+  return SRT3D_OK;
+}
+
 int srt3d_debug_phase_index(const uint16_t* bins, int64_t n, uint32_t T, uint32_t m, uint32_t* r, void* stream) {
   if (n < 0) return fail(SRT3D_EINVAL, "n=%lld < 0", (long long)n);
   if (T < 2 || T > SRT3D_MAX_T) return fail(SRT3D_EINVAL, "T=%u out of range", T);

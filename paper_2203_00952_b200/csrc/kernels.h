@@ -66,6 +66,7 @@ struct PixArgs {
 enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3 };
 
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms);
+cudaError_t measure_ffma_peak(double* tflops, int num_sms);
 cudaError_t launch_sketch_hist(int M, const SketchArgs& a, double mean_photons, cudaStream_t s, int num_sms);
 size_t sketch_hist_smem(uint32_t T, int M);
 cudaError_t launch_sketch_pair(int M, const SketchArgs& a, cudaStream_t s, int num_sms);

@@ -38,6 +38,47 @@ __global__ void check_csr_kernel(const uint16_t* __restrict__ bins, const uint32
   }
 }
 
+// K8: the FP32 FMA rate this GPU sustains right now — 8
+// independent FFMA chains per thread, 1024-thread CTAs, 4 per SM; the
+// roofline's "also measure it in the same run".
+__global__ void __launch_bounds__(1024) ffma_peak_kernel(float* out, float b, float c, int iters) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) v[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+#pragma unroll
+      for (int i = 0; i < 8; i++) v[i] = fmaf(v[i], b, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += v[i];
+  if (s == 12345.678f) out[0] = s;  // keeps the chains live
+}
+
+cudaError_t measure_ffma_peak(double* tflops, int num_sms) {
+  float* dummy = nullptr;
+  cudaEvent_t e0, e1;
+  cudaError_t e = cudaMalloc(&dummy, sizeof(float));
+  if (e != cudaSuccess) return e;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4096, blocks = num_sms * 2, threads = 1024;
+  ffma_peak_kernel<<<blocks, threads>>>(dummy, 0.999f, 1e-3f, 64);  // warm-up
+  cudaEventRecord(e0);
+  ffma_peak_kernel<<<blocks, threads>>>(dummy, 0.999f, 1e-3f, iters);
+  cudaEventRecord(e1);
+  e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  if (e == cudaSuccess) *tflops = 2.0 * 8 * 16 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(dummy);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms) {
   const bool tab = ((size_t)a.T + 1) * sizeof(float2) <= SK_MAX_SMEM;
   if (!tab) return launch_sketch_g32(M, false, a, s, num_sms);
