@@ -52,8 +52,10 @@ __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.
 // the padded shared tile with asynchronous copies (LDGSTS: every lane keeps
 // all its copies in flight; no register staging).  Units are 16 bytes (two
 // complex) when m is even, else 8 bytes.  Row/column advance incrementally.
+// v16 needs an even m AND a 16-byte-aligned slab (z itself may be only
+// 8-byte aligned: the ABI's requirement).
 __device__ __forceinline__ void warp_slab_issue(float2* tile, const float2* gsrc, int nrows, int m, int S, int lane) {
-  const bool v16 = (m & 1) == 0;
+  const bool v16 = (m & 1) == 0 && ((uintptr_t)gsrc & 15u) == 0;
   const int mu = v16 ? m / 2 : m;  // units per row
   const int total = nrows * mu;
   int row = lane / mu, col = lane - (lane / mu) * mu;
