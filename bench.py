@@ -129,7 +129,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ oracle (CPU)
-def oracle_step_sample(frame, seconds: float, rank0_only=True):
+def oracle_step_sample(frame, seconds: float, single_core: bool = False):
     """Time the fp64 oracle (as it stands) on a bounded sample of the frame:
     sketch of npix_s pixels + the config's iterations on those pixels."""
     import oracle
@@ -160,9 +160,29 @@ def oracle_step_sample(frame, seconds: float, rank0_only=True):
     if dt < seconds and n < frame.npix:
         n = min(frame.npix, max(n, int(n * seconds / max(dt, 1e-6))))
         dt, ph = run(n)
-    return {"seconds": dt, "photons": ph, "pixels": n, "cores": cores,
-            "sample": f"first {n} of {frame.npix} pixels ({ph} photons): oracle sketch + {frame.iters} "
-                      f"fp64 gradient/update iterations"}
+    out = {"seconds": dt, "photons": ph, "pixels": n, "cores": cores, "cpu_model": _cpu_model(),
+           "sample": f"first {n} of {frame.npix} pixels ({ph} photons): oracle sketch + {frame.iters} "
+                     f"fp64 gradient/update iterations"}
+    if single_core and cores > 1:  # also one core, on a proportionally smaller sample
+        oracle.set_threads(1)
+        try:
+            n1 = max(1, n // cores)
+            dt1, ph1 = run(n1)
+            out["one_core"] = {"value": ph1 / dt1, "unit": "photons/s", "pixels": n1, "seconds": dt1}
+        finally:
+            oracle.set_threads(cores)
+    return out
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def make_frame(args, rank: int):
@@ -207,7 +227,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_obj(f, args),
             "cpu_baseline": {"value": value, "unit": "photons/s", "cores": info["cores"], "kind": "oracle",
-                             "sample": info["sample"]},
+                             "sample": info["sample"], "cpu_model": info["cpu_model"]},
             "e2e": {"value": value, "unit": "photons/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -508,9 +528,10 @@ def run_srt3d(args):
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        info = oracle_step_sample(f, args.cpu_seconds)
+        info = oracle_step_sample(f, args.cpu_seconds, single_core=True)
         cpu = {"value": info["photons"] / info["seconds"], "unit": "photons/s", "cores": info["cores"],
-               "kind": "oracle", "sample": info["sample"]}
+               "kind": "oracle", "sample": info["sample"], "cpu_model": info["cpu_model"],
+               "one_core": info.get("one_core")}
 
     line = {"metric": METRIC, "value": photons_all / (ms_max * 1e-3), "unit": "photons/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
