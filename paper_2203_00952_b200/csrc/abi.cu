@@ -102,7 +102,9 @@ int choose_path(uint32_t T, uint32_t m, double mean, int* lanes) {
   const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
   int path = SRT3D_PATH_DIRECT;
   if (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) path = SRT3D_PATH_BINCOUNT;
-  if (lanes) *lanes = path == SRT3D_PATH_BINCOUNT ? 0 : (path == SRT3D_PATH_PAIRED ? 32 : lanes_for(mean));
+  int G = lanes_for(mean);
+  if (G == 8 && M0 >= 24) G = 4;  // the G = 4 rotated-Chebyshev regime of srt3d_sketch_ex
+  if (lanes) *lanes = path == SRT3D_PATH_BINCOUNT ? 0 : (path == SRT3D_PATH_PAIRED ? 32 : G);
   return path;
 }
 
@@ -159,9 +161,12 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   for (uint32_t j0 = 0; j0 < m; j0 += 32) {
     a.j0 = j0;
     const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
+    // auto regime, long passes at ~1e3 photons/pixel: G = 4 + rotated
+    // Chebyshev beats G = 8 + complex power
+    const int Gp = (lanes_per_pixel == 0 && G == 8 && M >= 24) ? srt3d::SK_G4_CHEB : G;
     cudaError_t e = path == SRT3D_PATH_BINCOUNT ? srt3d::launch_sketch_hist(M, a, mean, s, nsm)
                     : path == SRT3D_PATH_PAIRED ? srt3d::launch_sketch_pair(M, a, s, nsm)
-                                                : srt3d::launch_sketch_pass(M, G, a, s, nsm);
+                                                : srt3d::launch_sketch_pass(M, Gp, a, s, nsm);
     if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
   }
   return SRT3D_OK;

@@ -10,6 +10,7 @@ constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T < 24576 
 #ifndef SK_SCHEME
 #define SK_SCHEME 0                              // grouped direct path phasor scheme: 0 complex power, 1 rotated Chebyshev (selects)
 #endif
+constexpr int SK_G4_CHEB = -4;                  // launch_sketch_pass regime: G = 4 with the rotated Chebyshev scheme
 constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 #ifndef GRAD_THREADS
 #define GRAD_THREADS 64                          // gradient-kernel CTA size (one warp = 32 pixels)

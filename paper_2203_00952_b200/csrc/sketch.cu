@@ -10,6 +10,7 @@ cudaError_t launch_sketch_g4(int M, bool tab, const SketchArgs& a, cudaStream_t 
 cudaError_t launch_sketch_g8(int M, bool tab, const SketchArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_sketch_g16(int M, bool tab, const SketchArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_sketch_g32(int M, bool tab, const SketchArgs& a, cudaStream_t s, int num_sms);
+cudaError_t launch_sketch_g4_cheb(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
 
 // ---- debug / validation kernels -----------------------------------------
 __global__ void phase_index_kernel(const uint16_t* __restrict__ bins, long long n, uint32_t T, uint32_t m,
@@ -82,6 +83,7 @@ cudaError_t measure_ffma_peak(double* tflops, int num_sms) {
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms) {
   const bool tab = ((size_t)a.T + 1) * sizeof(float2) <= SK_MAX_SMEM;
   if (!tab) return launch_sketch_g32(M, false, a, s, num_sms);
+  if (G == SK_G4_CHEB) return launch_sketch_g4_cheb(M, a, s, num_sms);
   switch (G) {
     case 4:
       return launch_sketch_g4(M, true, a, s, num_sms);

@@ -58,9 +58,7 @@ int main() {
     double ph = (double)npix * n;
     if (frame == 0) {
       run<32, 8, 0>("C5like", a, nsm, ph, ref, dz, zn);
-      run<32, 4, 0>("C5like", a, nsm, ph, ref, dz, zn);
-      run<32, 16, 0>("C5like", a, nsm, ph, ref, dz, zn);
-      run<32, 8, 1>("C5like", a, nsm, ph, ref, dz, zn);
+      run<32, 4, 1>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 4, 1>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 16, 1>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 8, 2>("C5like", a, nsm, ph, ref, dz, zn);
