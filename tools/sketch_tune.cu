@@ -59,6 +59,9 @@ int main() {
     if (frame == 0) {
       run<32, 8, 0>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 4, 1>("C5like", a, nsm, ph, ref, dz, zn);
+      run<32, 2, 1>("C5like", a, nsm, ph, ref, dz, zn);
+      run<32, 1, 1>("C5like", a, nsm, ph, ref, dz, zn);
+      run<32, 2, 0>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 4, 1>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 16, 1>("C5like", a, nsm, ph, ref, dz, zn);
       run<32, 8, 2>("C5like", a, nsm, ph, ref, dz, zn);
