@@ -248,9 +248,13 @@ __global__ void __launch_bounds__(BP_WARPS * 32) init_k1_kernel(const BpArgs a) 
 cudaError_t launch_init_k1(const BpArgs& a, cudaStream_t s) {
   if (a.npix <= 0) return cudaSuccess;
   const size_t smem = sizeof(float2) * BP_WARPS * 32 * (a.m | 1u);
-  cudaError_t e = cudaFuncSetAttribute(init_k1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(float2) * BP_WARPS * 32 * (MAX_M | 1)));
-  if (e != cudaSuccess) return e;
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(init_k1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(float2) * BP_WARPS * 32 * (MAX_M | 1)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   const long long grid = (a.npix + 32 * BP_WARPS - 1) / (32 * BP_WARPS);
   init_k1_kernel<<<(unsigned)grid, BP_WARPS * 32, smem, s>>>(a);
   return cudaGetLastError();
@@ -264,12 +268,18 @@ cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int n
   if (a.npix <= 0) return cudaSuccess;
   const size_t smem = backproject_smem(a.N, pick);
   auto fn = pick ? backproject_kernel<true> : backproject_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static bool attr_set[2] = {false, false};  // benign race: idempotent
+  if (!attr_set[pick]) {
+    // the largest grid the entry points accept: N <= 8192 (backproject), N <= 4096 (picks)
+    const size_t cap = pick ? backproject_smem(4096, true) : backproject_smem(8192, false);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    if (e != cudaSuccess) return e;
+    attr_set[pick] = true;
+  }
+  static OccCache occ[2];
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BP_WARPS * 32, smem);
+  cudaError_t e = occupancy_cached(occ[pick], fn, BP_WARPS * 32, smem, &per_sm);
   if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
   long long grid = (a.npix + BP_WARPS - 1) / BP_WARPS;
   const long long cap = (long long)per_sm * num_sms;
   if (grid > cap) grid = cap;

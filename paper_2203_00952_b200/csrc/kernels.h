@@ -66,6 +66,30 @@ struct PixArgs {
 
 enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3 };
 
+// Host-side cache of the resident-CTA count of one kernel for the last
+// dynamic shared-memory size asked for (the occupancy query costs several
+// microseconds per launch otherwise).  Races are benign: a stale or torn
+// value only changes a persistent grid's size, never a result.
+struct OccCache {
+  size_t smem = ~(size_t)0;
+  int per_sm = 0;
+};
+template <typename F>
+inline cudaError_t occupancy_cached(OccCache& c, F fn, int threads, size_t smem, int* per_sm) {
+  if (c.smem == smem && c.per_sm > 0) {
+    *per_sm = c.per_sm;
+    return cudaSuccess;
+  }
+  int v = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (v < 1) v = 1;
+  c.per_sm = v;
+  c.smem = smem;
+  *per_sm = v;
+  return cudaSuccess;
+}
+
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms);
 cudaError_t measure_ffma_peak(double* tflops, int num_sms);
 cudaError_t launch_sketch_hist(int M, const SketchArgs& a, double mean_photons, cudaStream_t s, int num_sms);

@@ -182,8 +182,9 @@ static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sm
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  static OccCache occ;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, HS_THREADS, smem);
+  cudaError_t e = occupancy_cached(occ, fn, HS_THREADS, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   long long grid = (long long)per_sm * num_sms;

@@ -374,8 +374,9 @@ static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  static OccCache occ;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SK_THREADS, smem);
+  cudaError_t e = occupancy_cached(occ, fn, SK_THREADS, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   constexpr int PPW = 32 / G;

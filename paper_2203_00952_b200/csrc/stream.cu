@@ -474,13 +474,18 @@ static cudaError_t launch_bucket_two_level(const uint32_t* pix, const uint16_t* 
   if (fg > (long long)num_sms * 16) fg = (long long)num_sms * 16;
   scan_add_kernel<<<(unsigned)fg, 256, 0, s>>>(table, bsum, tn, misc + 1);
   const size_t psmem = sizeof(uint32_t) * BK_TILE + sizeof(uint16_t) * BK_TILE;
-  e = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-  if (e != cudaSuccess) return e;
+  static bool attr_set = false;  // benign race: idempotent (both attributes use their maximum sizes)
+  if (!attr_set) {
+    e = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(bucket_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(uint32_t) * ((size_t)2 * (1u << BK_MAX_S) + BK_TILE)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   if (nch > 0) partition_kernel<<<(unsigned)nch, 1024, psmem, s>>>(pix, bins, nev, npix, S, NB, nch, table, temp);
   // with no events the table is all zeros: pass C writes zero offsets
   const size_t smem = sizeof(uint32_t) * ((size_t)2 * (1u << S) + BK_TILE);
-  e = cudaFuncSetAttribute(bucket_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   bucket_fine_kernel<<<(unsigned)NB, 1024, smem, s>>>(temp, table, npix, S, nchv, NB, offsets, bins_out);
   if (dropped_out) {
     e = cudaMemcpyAsync(dropped_out, misc, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
