@@ -2,14 +2,17 @@
  * srt3d.h — C ABI of libsrt3d.so, the B200 (sm_100a) hot path of sketched
  * RT3D (SRT3D, arxiv 2203.00952).
  *
- * Citations: "PAPER.md:n" = line n of the paper text; readings A1..A17 of
- * ambiguous passages are listed in DESIGN.md §3.
+ * Citations: "PAPER.md:n" = line n of the paper text, "SPEC.md:n" = line n
+ * of the CPU-program specification written from it; readings A1..A21 of
+ * ambiguous or silent passages are listed in DESIGN.md §3.
  *
  * Conventions shared by every entry point
  * ---------------------------------------
  *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA
- *    tensors).  The caller owns every buffer; the library allocates no device
- *    memory and keeps no pointer after the call returns.
+ *    tensors).  The caller owns every buffer (workspace included, e.g. the
+ *    bucketing scratch); the library allocates no device memory (except the
+ *    measurement utility srt3d_debug_ffma_peak) and keeps no pointer after the
+ *    call returns.
  *  - Calls are asynchronous and stream-ordered: work is enqueued on `stream`
  *    (a cudaStream_t; NULL = the legacy default stream) and the function
  *    returns.  Outputs are valid once the stream has synchronised.  Every
@@ -28,8 +31,10 @@
  *    srt3d_check_csr): 0 <= bins[p] < T, offsets non-decreasing,
  *    offsets[npix] - offsets[0] < 2^32.  Violations give unspecified values
  *    but never reads outside bins[offsets[0] .. offsets[npix]).
- *  - Inputs and outputs must not alias, except that srt3d_descent_update
- *    updates t and alpha in place.
+ *  - Inputs and outputs must not alias, except where an entry point says so
+ *    (srt3d_descent_update / srt3d_sketch_grad_step / srt3d_fit_pixelwise
+ *    update t and alpha in place; srt3d_sketch_merge may write over z_a or
+ *    z_b; srt3d_sketch_accumulate updates (z, n) in place).
  */
 #ifndef SRT3D_H_
 #define SRT3D_H_
