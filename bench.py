@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="frames in the e2e timed region (default: --steps)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pixel blocks pipelined H2D/compute in the e2e path")
     ap.add_argument("--no-init", action="store_true", help="skip the NEXT-3 initialisation timings")
     ap.add_argument("--init-grid", type=int, default=0, help="backprojection grid points (default 16 m)")
@@ -301,13 +301,14 @@ def run_srt3d(args):
         t0_p, a0_p = t0_h.pin_memory(), a0_h.pin_memory()
         t_out, a_out = torch.empty_like(t0_p).pin_memory(), torch.empty_like(a0_p).pin_memory()
         pipe.run_host(bins_p, offs_p, t0_p, a0_p, t_out, a_out, chunks=args.e2e_chunks)
+        pipe.run_host(bins_p, offs_p, t0_p, a0_p, t_out, a_out, chunks=args.e2e_chunks, chain=True)
         s.synchronize()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        for _ in range(args.e2e_steps):
-            pipe.run_host(bins_p, offs_p, t0_p, a0_p, t_out, a_out, chunks=args.e2e_chunks)
+        for k in range(args.e2e_steps):  # frames stream back to back (chain): PCIe stays busy
+            pipe.run_host(bins_p, offs_p, t0_p, a0_p, t_out, a_out, chunks=args.e2e_chunks, chain=k > 0)
         e1.record(s)
         s.synchronize()
         barrier()
@@ -317,8 +318,9 @@ def run_srt3d(args):
         e2e = {"value": f.n_photons * args.e2e_steps * world / (float(e2e_ms.item()) * 1e-3), "unit": "photons/s",
                "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
                "ms_per_step": float(e2e_ms.item()) / args.e2e_steps, "chunks": args.e2e_chunks,
-               "note": "pinned H2D of the frame + theta0, sketch + iterations, D2H of theta; pixel blocks "
-                       "pipelined (copy engine uploads block c+1 while block c computes)"}
+               "note": "pinned H2D of the frame + theta0, sketch + iterations, D2H of theta, every step; pixel "
+                       "blocks pipelined (copy engine uploads block c+1 while block c computes) and frames "
+                       "chained (frame f+1's uploads overlap frame f's last block)"}
 
     # L2-cold per-launch time of the gradient kernel (outside the timed region):
     # flush L2 by READING a buffer of 2x its size (leaves clean lines: no

@@ -15,7 +15,10 @@ costs two graph launches instead of 1 + iters kernel launches from Python.
                           pixel blocks (pixels are independent): the copy
                           engine uploads block c+1 on its own stream while
                           the SMs sketch and iterate block c (one CUDA graph
-                          per block), so PCIe and compute overlap.
+                          per block), so PCIe and compute overlap;
+                          chain=True lets consecutive frames stream back
+                          to back (frame f+1's uploads overlap frame f's
+                          last block).
 """
 from __future__ import annotations
 
@@ -140,13 +143,20 @@ class FramePipeline:
             ev.record(self.stream)
         self.stream.synchronize()
 
-    def run_host(self, bins_h, offsets_h, t0_h, a0_h, t_out_h, a_out_h, chunks: int = 1):
+    def run_host(self, bins_h, offsets_h, t0_h, a0_h, t_out_h, a_out_h, chunks: int = 1, chain: bool = False):
         """End-to-end step from (pinned) host buffers; results land in t_out_h / a_out_h.
-        chunks > 1: pipelined per pixel block (H2D of block c+1 overlaps compute of block c)."""
+        chunks > 1: pipelined per pixel block (H2D of block c+1 overlaps compute of block c).
+        chain=True (only directly after a chunked run_host with the same chunks, nothing else
+        enqueued on this pipeline in between): the uploads of this frame do not wait for the
+        previous frame's tail — block c is uploaded as soon as block c of the previous frame is
+        done (ev_done[c]), so consecutive frames stream back to back over PCIe."""
         if chunks > 1:
-            self.capture_chunks(chunks)
-            b = self.chunk_bounds
-            self.copy_stream.wait_stream(self.stream)  # uploads start after work already queued (and timers)
+            if chain and self.chunk_bounds is not None and len(self.chunk_bounds) - 1 == max(1, min(int(chunks), self.npix)):
+                b = self.chunk_bounds
+            else:
+                self.capture_chunks(chunks)
+                b = self.chunk_bounds
+                self.copy_stream.wait_stream(self.stream)  # uploads start after work already queued (and timers)
             for c in range(len(b) - 1):
                 i0, i1 = b[c], b[c + 1]
                 p0, p1 = int(offsets_h[i0]), int(offsets_h[i1])

@@ -521,3 +521,36 @@ def test_config_parity_full_size(gpu, oracle_mod, inputs_mod, name, n):
         go = oracle_mod.sketch_grad(zg[idx], t0[idx], a0[idx], f.sigma, f.T, f.m)
         _grad_tol_check(zg[idx], t0[idx], a0[idx], f.sigma, f.T, f.m,
                         (_host(gt)[idx], _host(ga)[idx], _host(L)[idx]), go)
+
+
+def test_pipeline_chained_frames(gpu, inputs_mod):
+    """run_host(chain=True): two different frames enqueued back to back (frame B's uploads
+    overlap frame A's last block, no host sync in between) each return bitwise the theta of
+    run_device on that frame — the per-block events order B's uploads after A's use of them."""
+    import torch
+
+    from paper_2203_00952_b200.pipeline import FramePipeline
+
+    fa = inputs_mod.make_frame("C2", rows=64, cols=61, seed=7)
+    fb = inputs_mod.make_frame("C2", rows=64, cols=61, seed=8)
+    nph = max(fa.n_photons, fb.n_photons)
+    pipe = FramePipeline(nph, fa.npix, fa.K, fa.T, fa.m, fa.sigma, iters=9)
+    refs, pins = [], []
+    for f, dt in ((fa, 0.0), (fb, 3.0)):
+        t0, a0 = f.theta0()
+        t0 = (t0 + np.float32(dt)).astype(np.float32)
+        pipe.load_device(_dev(f.bins), _dev(f.offsets), _dev(t0), _dev(a0))
+        if pipe.g_iter is None:
+            pipe.capture()
+        pipe.run_device()
+        pipe.stream.synchronize()
+        refs.append((_host(pipe.t).copy(), _host(pipe.a).copy()))
+        pins.append([torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (f.bins, f.offsets, t0, a0)])
+    outs = [(torch.zeros_like(p[2]).pin_memory(), torch.zeros_like(p[3]).pin_memory()) for p in pins]
+    for rep in range(2):
+        for k, (p, o) in enumerate(zip(pins, outs)):
+            pipe.run_host(*p, *o, chunks=5, chain=(k > 0 or rep > 0))
+        torch.cuda.synchronize()
+        for (t_ref, a_ref), (t_out, a_out) in zip(refs, outs):
+            assert np.array_equal(t_out.numpy().view(np.uint32), t_ref.view(np.uint32))
+            assert np.array_equal(a_out.numpy().view(np.uint32), a_ref.view(np.uint32))
