@@ -280,13 +280,13 @@ __global__ void __launch_bounds__(512) coarse_count_kernel(const uint32_t* __res
 // Pass B: the chunk again, in tiles of BK_TILE events counting-sorted by
 // bucket in shared memory, then written out in bucket order: consecutive
 // threads store consecutive addresses of a (bucket, chunk) segment.
-__device__ uint32_t block_scan_smem(uint32_t* a, int n, uint32_t* wsum);
+__device__ uint32_t block_scan_smem(uint32_t* a, uint32_t* out, int n, uint32_t* wsum);
 
 __global__ void __launch_bounds__(1024) partition_kernel(const uint32_t* __restrict__ pix,
                                                          const uint16_t* __restrict__ bins, unsigned long long nev,
                                                          long long npix, int S, int NB, long long nch,
                                                          const uint32_t* table, uint32_t* temp) {
-  __shared__ uint32_t cur[BK_MAX_BUCKETS], tc[BK_MAX_BUCKETS], wsum[32];
+  __shared__ uint32_t cur[BK_MAX_BUCKETS], tc[BK_MAX_BUCKETS], toff[BK_MAX_BUCKETS], wsum[32];
   extern __shared__ uint32_t pt_smem[];
   uint32_t* sbuf = pt_smem;                                        // [BK_TILE] packed values
   uint16_t* skey = reinterpret_cast<uint16_t*>(pt_smem + BK_TILE);  // [BK_TILE] bucket
@@ -294,30 +294,42 @@ __global__ void __launch_bounds__(1024) partition_kernel(const uint32_t* __restr
     cur[b] = table[(long long)b * nch + blockIdx.x];
     tc[b] = 0u;
   }
-  __syncthreads();
   const unsigned long long c0 = (unsigned long long)blockIdx.x * BK_CHUNK;
   const unsigned long long c1 = min(nev, c0 + BK_CHUNK);
   const uint32_t mask = (1u << S) - 1u;
   constexpr int PER = BK_TILE / 1024;
+  // the next tile's events are loaded while the current one is sorted and written
+  uint32_t np[PER], nb[PER];
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const unsigned long long e = c0 + threadIdx.x + q * 1024;
+    np[q] = e < c1 ? __ldcs(pix + e) : 0xffffffffu;
+    nb[q] = e < c1 ? (uint32_t)__ldcs(bins + e) : 0u;
+  }
+  __syncthreads();
   for (unsigned long long t0 = c0; t0 < c1; t0 += BK_TILE) {
     uint32_t key[PER], val[PER], rk[PER];
 #pragma unroll
-    for (int q = 0; q < PER; q++) {  // all loads of the tile in flight
-      const unsigned long long e = t0 + threadIdx.x + q * 1024;
-      const uint32_t p = e < c1 ? __ldcs(pix + e) : 0xffffffffu;
-      val[q] = e < c1 ? (uint32_t)__ldcs(bins + e) : 0u;
+    for (int q = 0; q < PER; q++) {
+      const uint32_t p = np[q];
       key[q] = (long long)p < npix ? (p >> S) : 0xffffffffu;
-      val[q] |= (p & mask) << 16;
+      val[q] = nb[q] | ((p & mask) << 16);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+      const unsigned long long e = t0 + BK_TILE + threadIdx.x + q * 1024;
+      np[q] = e < c1 ? __ldcs(pix + e) : 0xffffffffu;
+      nb[q] = e < c1 ? (uint32_t)__ldcs(bins + e) : 0u;
     }
 #pragma unroll
     for (int q = 0; q < PER; q++) rk[q] = key[q] != 0xffffffffu ? atomicAdd(&tc[key[q]], 1u) : 0u;
     __syncthreads();
-    const uint32_t nt = block_scan_smem(tc, NB, wsum);  // tile offsets per bucket; kept events in the tile
+    const uint32_t nt = block_scan_smem(tc, toff, NB, wsum);  // toff: tile offsets per bucket (tc keeps counts)
 #pragma unroll
     for (int q = 0; q < PER; q++)
       if (key[q] != 0xffffffffu) {
-        sbuf[tc[key[q]] + rk[q]] = val[q];
-        skey[tc[key[q]] + rk[q]] = (uint16_t)key[q];
+        sbuf[toff[key[q]] + rk[q]] = val[q];
+        skey[toff[key[q]] + rk[q]] = (uint16_t)key[q];
       }
     __syncthreads();
 #pragma unroll
@@ -325,22 +337,21 @@ __global__ void __launch_bounds__(1024) partition_kernel(const uint32_t* __restr
       const uint32_t i = threadIdx.x + q * 1024;
       if (i < nt) {
         const uint32_t b = skey[i];
-        temp[cur[b] + i - tc[b]] = sbuf[i];
+        temp[cur[b] + i - toff[b]] = sbuf[i];
       }
     }
     __syncthreads();
     for (int b = threadIdx.x; b < NB; b += blockDim.x) {
-      const uint32_t nxt = b + 1 < NB ? tc[b + 1] : nt;
-      cur[b] += nxt - tc[b];
+      cur[b] += tc[b];
+      tc[b] = 0u;
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < NB; b += blockDim.x) tc[b] = 0u;
     __syncthreads();
   }
 }
 
-// Exclusive block scan of n <= 8192 shared words (in place); returns the total.
-__device__ uint32_t block_scan_smem(uint32_t* a, int n, uint32_t* wsum) {
+// Exclusive block scan of n <= 8192 shared words: out[i] = sum_{k<i} a[k]
+// (out may alias a); returns the total.
+__device__ uint32_t block_scan_smem(uint32_t* a, uint32_t* out, int n, uint32_t* wsum) {
   const int per = (n + blockDim.x - 1) / blockDim.x;  // contiguous run per thread
   const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
   uint32_t t = 0;
@@ -369,23 +380,26 @@ __device__ uint32_t block_scan_smem(uint32_t* a, int n, uint32_t* wsum) {
   const uint32_t total = wsum[(blockDim.x >> 5) - 1];
   for (int i = lo; i < hi; i++) {
     const uint32_t v = a[i];
-    a[i] = run;
+    out[i] = run;
     run += v;
   }
   __syncthreads();
   return total;
 }
 
-// Pass C: one CTA per bucket — per-pixel offsets, then tile-sorted coalesced output.
+// Pass C: one CTA per bucket — per-pixel offsets, then tile-sorted coalesced
+// output; the next tile's events are loaded while the current one is sorted.
 __global__ void __launch_bounds__(1024) bucket_fine_kernel(const uint32_t* __restrict__ temp, const uint32_t* table,
                                                           long long npix, int S, long long nch, int NB,
                                                           uint32_t* offsets, uint16_t* out) {
   extern __shared__ uint32_t bk_smem[];
   const int P = 1 << S;
   uint32_t* cur = bk_smem;           // [P] global cursor of each local pixel
-  uint32_t* tc = cur + P;            // [P] tile counts -> tile offsets
-  uint32_t* sbuf = tc + P;           // [BK_TILE] tile sorted
+  uint32_t* tc = cur + P;            // [P] tile counts
+  uint32_t* toff = tc + P;           // [P] tile offsets
+  uint32_t* sbuf = toff + P;         // [BK_TILE] tile sorted
   __shared__ uint32_t wsum[32];
+  constexpr int PER = BK_TILE / 1024;
   const int b = blockIdx.x;
   const uint32_t bs = table[(long long)b * nch], be = table[(long long)(b + 1) * nch];
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -404,8 +418,15 @@ __global__ void __launch_bounds__(1024) bucket_fine_kernel(const uint32_t* __res
     for (int q = 0; q < 8; q++)
       if (w[q] != 0xffffffffu) atomicAdd(&cur[w[q] >> 16], 1u);
   }
+  // first tile's loads in flight across the scan
+  uint32_t nv[PER];
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const uint32_t i = bs + threadIdx.x + q * 1024;
+    nv[q] = i < be ? __ldcs(temp + i) : 0u;
+  }
   __syncthreads();
-  block_scan_smem(cur, P, wsum);
+  block_scan_smem(cur, cur, P, wsum);
   const long long p0 = (long long)b << S;
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     cur[i] += bs;
@@ -415,39 +436,41 @@ __global__ void __launch_bounds__(1024) bucket_fine_kernel(const uint32_t* __res
   __syncthreads();
   for (uint32_t t0 = bs; t0 < be; t0 += BK_TILE) {
     const int nt = (int)min((uint32_t)BK_TILE, be - t0);
-    uint32_t v[BK_TILE / 1024], r[BK_TILE / 1024];
+    uint32_t v[PER], r[PER];
 #pragma unroll
-    for (int q = 0; q < BK_TILE / 1024; q++) {
+    for (int q = 0; q < PER; q++) v[q] = nv[q];
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+      const uint32_t i = t0 + BK_TILE + threadIdx.x + q * 1024;
+      nv[q] = i < be ? __ldcs(temp + i) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
       const int i = threadIdx.x + q * 1024;
-      v[q] = i < nt ? temp[t0 + i] : 0u;
       r[q] = i < nt ? atomicAdd(&tc[v[q] >> 16], 1u) : 0u;
     }
     __syncthreads();
-    block_scan_smem(tc, P, wsum);  // tc: tile offsets of every local pixel
+    block_scan_smem(tc, toff, P, wsum);  // toff: tile offsets of every local pixel (tc keeps counts)
 #pragma unroll
-    for (int q = 0; q < BK_TILE / 1024; q++) {
+    for (int q = 0; q < PER; q++) {
       const int i = threadIdx.x + q * 1024;
-      if (i < nt) sbuf[tc[v[q] >> 16] + r[q]] = v[q];
+      if (i < nt) sbuf[toff[v[q] >> 16] + r[q]] = v[q];
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < BK_TILE / 1024; q++) {
+    for (int q = 0; q < PER; q++) {
       const int i = threadIdx.x + q * 1024;
       if (i < nt) {
         const uint32_t w = sbuf[i];
         const uint32_t lp = w >> 16;
-        out[cur[lp] + (uint32_t)i - tc[lp]] = (uint16_t)(w & 0xffffu);  // consecutive i, same pixel: consecutive addresses
+        out[cur[lp] + (uint32_t)i - toff[lp]] = (uint16_t)(w & 0xffffu);  // consecutive i, same pixel: consecutive addresses
       }
     }
     __syncthreads();
-    // advance the cursors by this tile's counts (tc holds offsets: count = next offset - offset)
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
-      const uint32_t nxt = i + 1 < P ? tc[i + 1] : (uint32_t)nt;
-      r[0] = nxt - tc[i];
-      cur[i] += r[0];
+      cur[i] += tc[i];
+      tc[i] = 0u;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < P; i += blockDim.x) tc[i] = 0u;
     __syncthreads();
   }
 }
@@ -479,13 +502,13 @@ static cudaError_t launch_bucket_two_level(const uint32_t* pix, const uint16_t* 
     e = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(bucket_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(uint32_t) * ((size_t)2 * (1u << BK_MAX_S) + BK_TILE)));
+                             (int)(sizeof(uint32_t) * ((size_t)3 * (1u << BK_MAX_S) + BK_TILE)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   if (nch > 0) partition_kernel<<<(unsigned)nch, 1024, psmem, s>>>(pix, bins, nev, npix, S, NB, nch, table, temp);
   // with no events the table is all zeros: pass C writes zero offsets
-  const size_t smem = sizeof(uint32_t) * ((size_t)2 * (1u << S) + BK_TILE);
+  const size_t smem = sizeof(uint32_t) * ((size_t)3 * (1u << S) + BK_TILE);
   bucket_fine_kernel<<<(unsigned)NB, 1024, smem, s>>>(temp, table, npix, S, nchv, NB, offsets, bins_out);
   if (dropped_out) {
     e = cudaMemcpyAsync(dropped_out, misc, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);

@@ -36,7 +36,7 @@ def _events(npix, T, n_ev, seed, extra_bad=0):
 @pytest.mark.parametrize("npix,T,n_ev,bad", [(1000, 4096, 200000, 0), (262144, 8192, 1000000, 17),
                                              (5000, 1024, 0, 0), (1, 100, 5000, 3), (70000, 2500, 300000, 0),
                                              (513, 4096, 40000, 5), (4194304, 1024, 300000, 0),
-                                             (5000000, 2048, 200000, 2)])
+                                             (5000000, 2048, 200000, 2), (9000000, 1024, 100000, 1)])
 def test_bucket_events_parity(gpu, oracle_mod, npix, T, n_ev, bad):
     import torch
 
