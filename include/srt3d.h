@@ -99,10 +99,12 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  *                   histogram h[x] then z_j = (1/n) sum_x h[x] e^{i 2 pi j x/T}
  *                   (the same sum as Eq. (3) regrouped by bin; T <= ~17000,
  *                   else SRT3D_EUNSUPPORTED);
- *                   SRT3D_PATH_PAIRED (3): the direct sum, one warp per pixel,
- *                   photons sorted by phase class into (A, B) pairs that run
- *                   the rotated Chebyshev recurrence (
- *                   T < 24576, else SRT3D_EUNSUPPORTED).
+ *                   SRT3D_PATH_PAIRED (3): the direct sum, four lanes per
+ *                   pixel, each chunk of <= 256 photons staged in shared
+ *                   memory partitioned by phase class, then class-uniform
+ *                   rotated Chebyshev loops with one accumulator frame switch
+ *                   per class (T <= 23800, else
+ *                   SRT3D_EUNSUPPORTED).
  *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path only).
  */
 #define SRT3D_PATH_AUTO 0

@@ -95,7 +95,7 @@ int lanes_for(double mean_photons) {
   return 4;
 }
 
-bool pair_fits(uint32_t T) { return ((size_t)T + 1) * sizeof(float2) <= srt3d::SK_MAX_SMEM; }
+bool pair_fits(uint32_t T) { return T <= srt3d::SO_MAX_T; }
 
 int choose_path(uint32_t T, uint32_t m, double mean, int* lanes) {
   const int M0 = (int)(m < 32 ? m : 32);
@@ -135,7 +135,7 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
   if (path == SRT3D_PATH_BINCOUNT && !hist_fits)
     return fail(SRT3D_EUNSUPPORTED, "bin-count path needs T <= ~17000 (T=%u)", T);
   if (path == SRT3D_PATH_PAIRED && !pair_fits(T))
-    return fail(SRT3D_EUNSUPPORTED, "paired path needs T < 24576 (T=%u)", T);
+    return fail(SRT3D_EUNSUPPORTED, "class-sorted path needs T <= %u (T=%u)", srt3d::SO_MAX_T, T);
   cudaStream_t s = (cudaStream_t)stream;
   uint64_t total = total_photons_hint;
   if (total == 0 && (path == SRT3D_PATH_AUTO || lanes_per_pixel == 0)) {

@@ -10,6 +10,7 @@ constexpr size_t SK_MAX_SMEM = 24576 * 8;       // phase-table bytes (T < 24576 
 #ifndef SK_SCHEME
 #define SK_SCHEME 0                              // grouped direct path phasor scheme: 0 complex power, 1 rotated Chebyshev (selects)
 #endif
+constexpr uint32_t SO_MAX_T = 23800;             // class-sorted path: phase table + per-group photon buffers fit 227 KB
 constexpr int SK_G4_CHEB = -4;                  // launch_sketch_pass regime: G = 4 with the rotated Chebyshev scheme
 constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 #ifndef GRAD_THREADS

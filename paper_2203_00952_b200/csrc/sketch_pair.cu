@@ -1,30 +1,32 @@
-// K1 paired path (SRT3D_PATH_PAIRED) — photon -> sketch accumulator, Eq. (3)
-// (PAPER.md:59-63), for pixels with hundreds of photons or more.
+// K1 class-sorted path (SRT3D_PATH_PAIRED) — photon -> sketch accumulator,
+// Eq. (3), for pixels with hundreds of photons or more.
 //
 //   z[i][j-1] = (1/n_i) sum_p exp(i 2 pi j x_p / T),  j = j0+1 .. j0+M
 //
-// Why a second direct kernel: on sm_100a the direct sum is
-// bound by register-file operand reads, not by FP32 lanes.  A packed FP32x2
-// instruction costs max(2, #distinct even regs, #distinct odd regs) issue
-// cycles, so the complex-power recurrence (FMUL2 + FFMA2 + FADD2) costs ~7
-// cycles per (photon, j) per warp.  The rotated Chebyshev recurrence
+// Why: on sm_100a the direct sum is bound by register-file
+// operand reads, not by FP32 lanes.  A packed FP32x2 instruction costs
+// max(2, #distinct even regs, #distinct odd regs) issue cycles, so the
+// complex-power recurrence (FMUL2 + FFMA2 + FADD2) costs ~7 cycles per
+// (photon, j) per warp.  The rotated Chebyshev recurrence
 // v_j = 2 cos(theta') v_{j-1} - v_{j-2} needs one FFMA2 + one FADD2 (~5
-// cycles) — but only if the rotation class of every photon in an instruction
-// is known at compile time: a photon with |sin theta| < |cos theta| runs its
+// cycles) — if the rotation class of every photon in an instruction is known
+// at compile time: a photon with |sin theta| < |cos theta| (class B) runs its
 // chain on theta' = theta + pi/2 (exact: i * w, keeps |sin theta'| >= 1/sqrt2,
-// tools/sim_cheb_error.c) and its terms are rotated back by (-i)^j, which is a
-// free operand swizzle (.LO_HI / negate) only when it is uniform.
+// tools/sim_cheb_error.c) and its terms must be rotated back by (-i)^j.
 //
-// So each warp owns one pixel at a time and sorts the pixel's photons by
-// class into two shared-memory queues (A: |sin| >= |cos|, no rotation;
-// B: rotated).  Every step then processes one (A, B) pair per lane: slot x
-// always class A, slot y always class B, an empty queue supplying the absent
-// photon (zero table entry tab[T], zero seeds); two pairs per step (four
-// independent chains per lane).  Photons are read with
-// coalesced 16-byte loads (scalar head/tail peel to 16-byte alignment), the
-// class of bin x is an integer test on u = 2x mod T (B iff 4u < T or 4u > 3T),
-// and the warp-wide compaction is one packed shuffle scan per 256 photons.
-// Per-lane fp32 sums are folded every <= 256 photons per lane with the fixed-order
+// The back-rotation is linear, so it need not be applied per photon: a lane
+// that accumulates only class-B photons for a while can keep its accumulator
+// in the "B frame" acc'_j = i^j acc_j, add the raw chain values, and rotate
+// the whole accumulator back once (compile-time swizzles / negations per j).
+// So each group of G = 4 lanes (one pixel, as the grouped kernel) stages a
+// chunk of its pixel's photons (up to 256 + the head/tail peel) in shared
+// memory partitioned by class — class A from the front, class B from the
+// back, positions from a 4-lane shuffle scan of per-lane counts — then runs
+// all class-A photons, switches the frame, runs all class-B photons, and
+// switches back.  Both loops run the same class-uniform body (two photons
+// per step, two FFMA2 + two FADD2 per term); the class of bin x is an
+// integer test on u = 2x mod T (B iff 4u < T or 4u > 3T).  Per-lane fp32 sums
+// are folded after every chunk (<= 68 photons per lane) with the fixed-order
 // butterfly reduce-scatter (bitwise reproducible).
 #include <cstdint>
 #include <utility>
@@ -33,37 +35,59 @@
 
 namespace srt3d {
 
-constexpr int PQ_CAP = 512;                  // photons per class queue per warp (power of two)
-constexpr int PQ_SMEM_PER_WARP = 2 * (PQ_CAP + 8) * 2;  // + junk slots
+constexpr int SO_G = 4;                 // lanes per pixel
+constexpr int SO_SLOTS = 32;            // 16-byte slots (8 photons) per chunk per group: 8 per lane
+constexpr int SO_CAP = 328;             // staged photons per group: 256 + head/tail (< 16), padded so the
+                                        // group buffers start 4 banks apart (164 words = 4 mod 32)
+constexpr int SO_GROUPS = SK_THREADS / SO_G;
+constexpr int SO_JUNK = SO_CAP - 1;     // store target of invalid photons (branch-free append)
+constexpr int SO_BTOP = SO_CAP - 2;     // class B fills downwards from here
+
+// class of bin x (x < T <= 65536): B iff 4u < T or 4u > 3T, u = 2x mod T
+__device__ __forceinline__ uint32_t so_class_b(uint32_t x, uint32_t T) {
+  const uint32_t u2 = 2u * x;
+  const uint32_t u = min(u2, u2 - T);  // 2x mod T (the wrapped difference is larger when 2x < T)
+  return (4u * u - T) > 2u * T ? 1u : 0u;
+}
 
 template <int M>
-struct PairAcc {
+struct SortAcc {
   u64 acc[M];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = 0ull;
   }
-  // Term J of the pass for two (A, B) pairs: advance the four chains (J > 0)
-  // and accumulate xa0 + xa1 + (-i)^{1+J} (yb0 + yb1).
   template <int J>
-  __device__ __forceinline__ void term(Chain& x0, Chain& y0, Chain& x1, Chain& y1) {
+  __device__ __forceinline__ void term(Chain& x, Chain& y) {
     if constexpr (J > 0) {
-      x0.advance();
-      y0.advance();
-      x1.advance();
-      y1.advance();
+      x.advance();
+      y.advance();
     }
-    const u64 s0 = fadd2(x0.B, rot_back<J>(y0.B));
-    const u64 s1 = fadd2(x1.B, rot_back<J>(y1.B));
-    acc[J] = fadd2(acc[J], fadd2(s0, s1));
+    acc[J] = fadd2(acc[J], fadd2(x.B, y.B));
   }
   template <int... J>
-  __device__ __forceinline__ void terms(std::integer_sequence<int, J...>, Chain& x0, Chain& y0, Chain& x1,
-                                        Chain& y1) {
-    (term<J>(x0, y0, x1, y1), ...);
+  __device__ __forceinline__ void terms(std::integer_sequence<int, J...>, Chain& x, Chain& y) {
+    (term<J>(x, y), ...);
   }
-  // Chain seeds of photon x (T = absent) for the pass starting at j0 + 1;
-  // rotated (class B) chains run on i * w.
+  // acc_J *= i^r with r = (1 + J) (to the B frame) or 3 (1 + J) (back), mod 4
+  template <bool TO_B, int J>
+  __device__ __forceinline__ void rot1() {
+    constexpr int r = TO_B ? ((1 + J) & 3) : ((3 * (1 + J)) & 3);
+    const u64 v = acc[J];
+    if constexpr (r == 1) {
+      acc[J] = pk(-hi_of(v), lo_of(v));
+    } else if constexpr (r == 2) {
+      acc[J] = neg2(v);
+    } else if constexpr (r == 3) {
+      acc[J] = pk(hi_of(v), -lo_of(v));
+    }
+  }
+  template <bool TO_B, int... J>
+  __device__ __forceinline__ void frame(std::integer_sequence<int, J...>) {
+    (rot1<TO_B, J>(), ...);
+  }
+  // Chain seeds of photon x (T = absent: zero table entry, zero seeds) for the
+  // pass starting at j0 + 1; class-B chains run on i * w.
   template <bool ROT>
   __device__ __forceinline__ static Chain seed(const float2* tab, uint32_t x, uint32_t T, uint32_t j0, float invT) {
     const float2 w = tab[x];
@@ -81,77 +105,76 @@ struct PairAcc {
     }
     return c;
   }
-  // Two (A, B) pairs: xa* class A (or T = absent), xb* class B (or T).
-  __device__ __forceinline__ void pair2(const float2* tab, uint32_t xa0, uint32_t xb0, uint32_t xa1, uint32_t xb1,
-                                        uint32_t T, uint32_t j0, float invT) {
-    Chain x0 = seed<false>(tab, xa0, T, j0, invT), y0 = seed<true>(tab, xb0, T, j0, invT);
-    Chain x1 = seed<false>(tab, xa1, T, j0, invT), y1 = seed<true>(tab, xb1, T, j0, invT);
-    terms(std::make_integer_sequence<int, M>{}, x0, y0, x1, y1);
+  template <bool ROT>
+  __device__ __forceinline__ void pair(const float2* tab, uint32_t x, uint32_t y, uint32_t T, uint32_t j0,
+                                       float invT) {
+    Chain cx = seed<ROT>(tab, x, T, j0, invT), cy = seed<ROT>(tab, y, T, j0, invT);
+    terms(std::make_integer_sequence<int, M>{}, cx, cy);
   }
 };
 
-// Warp-wide append of the 8 photons in v (valid iff `valid`) to the class
-// queues; tA / tB are the warp-uniform tail counters.  Branch-free: invalid
-// lanes write to the junk slot qA[PQ_CAP].
-__device__ __forceinline__ void pq_append(uint16_t* qA, uint16_t* qB, const uint4 v, int nv, uint32_t T, int lane,
-                                          uint32_t& tA, uint32_t& tB) {
+// Append the photons of v (bit i of vmask: photon i valid; valid photons
+// first) to the group's class-partitioned buffer: class A at qb[fA ...),
+// class B at qb[SO_BTOP-fB ...) downwards.  fA / fB are group-uniform fill
+// counters.  Photon i goes to (B ? ob : oa + i) - (#B before i): no serial
+// counter chain, one predicated store per photon.
+__device__ __forceinline__ void so_append(uint16_t* qb, const uint4 v, uint32_t vmask, uint32_t T, int gl,
+                                          uint32_t& fA, uint32_t& fB) {
   const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
   uint32_t isb = 0;
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const uint32_t x = (wv[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-    isb |= (class_b(x, T) ? 1u : 0u) << i;
-  }
-  const uint32_t vmask = nv >= 8 ? 0xffu : ((1u << nv) - 1u);
+  for (int i = 0; i < 8; i++) isb |= so_class_b((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu, T) << i;
   isb &= vmask;
   const uint32_t nb = __popc(isb), na = (uint32_t)__popc(vmask) - nb;
   const uint32_t p = na | (nb << 16);
   uint32_t s = p;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, s, d);
-    if (lane >= d) s += t;
-  }
-  const uint32_t tot = __shfl_sync(0xffffffffu, s, 31);
+  uint32_t t = __shfl_up_sync(0xffffffffu, s, 1, SO_G);
+  if (gl >= 1) s += t;
+  t = __shfl_up_sync(0xffffffffu, s, 2, SO_G);
+  if (gl >= 2) s += t;
+  const uint32_t tot = __shfl_sync(0xffffffffu, s, SO_G - 1, SO_G);
   const uint32_t ex = s - p;
-  uint32_t oa = tA + (ex & 0xffffu), ob = tB + (ex >> 16);
+  const uint32_t oa = fA + (ex & 0xffffu), ob = (uint32_t)SO_BTOP - fB - (ex >> 16);
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const uint16_t x = (uint16_t)((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-    const bool b = (isb >> i) & 1u, ok = (vmask >> i) & 1u;
-    uint16_t* dst = !ok ? qA + PQ_CAP : (b ? qB + (ob & (PQ_CAP - 1)) : qA + (oa & (PQ_CAP - 1)));
-    *dst = x;
-    oa += (ok && !b) ? 1u : 0u;
-    ob += (ok && b) ? 1u : 0u;
+  for (int i = 0; i < 8; i++) {  // unconditional store: invalid photons go to the junk slot
+    const uint32_t nbefore = __popc(isb & ((1u << i) - 1u));
+    const uint32_t dst = (((isb >> i) & 1u) ? ob : oa + (uint32_t)i) - nbefore;
+    qb[((vmask >> i) & 1u) ? dst : (uint32_t)SO_JUNK] = (uint16_t)((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
   }
-  tA += tot & 0xffffu;
-  tB += tot >> 16;
+  fA += tot & 0xffffu;
+  fB += tot >> 16;
 }
 
 template <int M>
-__global__ void __launch_bounds__(SK_THREADS) sketch_pair_kernel(SketchArgs a) {
+__global__ void __launch_bounds__(SK_THREADS, 2) sketch_sorted_kernel(SketchArgs a) {
   extern __shared__ float2 tab[];
   build_phase_table(tab, a.T);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint16_t* qA = reinterpret_cast<uint16_t*>(tab + ((a.T + 2) & ~1u)) + warp * 2 * (PQ_CAP + 8);
-  uint16_t* qB = qA + PQ_CAP + 8;
+  const int lane = threadIdx.x & 31, gl = lane & (SO_G - 1), grp = lane / SO_G;
+  uint16_t* qb = reinterpret_cast<uint16_t*>(tab + ((a.T + 2) & ~1u)) + (size_t)(threadIdx.x / SO_G) * SO_CAP;
   __syncthreads();
 
+  constexpr int PPW = 32 / SO_G;
   constexpr int NV = 2 * M;
-  constexpr int NVP = ((NV + 31) / 32) * 32;
-  constexpr int VL = NVP / 32;
-  constexpr int FLUSH_STEPS = 64;  // <= 256 photons per lane per fp32 partial
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  constexpr int NVP = ((NV + SO_G - 1) / SO_G) * SO_G;
+  constexpr int VL = NVP / SO_G;
+  const long long warp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long ntiles = (a.npix + PPW - 1) / PPW;
   const uint32_t off0 = (uint32_t)(((uintptr_t)a.bins >> 1) & 7u);
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(a.bins - off0);
   const uint16_t* __restrict__ bins = a.bins;
   const uint32_t T = a.T, j0 = a.j0;
   const float invT = 1.0f / (float)a.T;
 
-  for (long long pix = gw; pix < a.npix; pix += nw) {
-    unsigned long long beg = a.offsets[pix], end = a.offsets[pix + 1];
-    if (end < beg) end = beg;  // malformed CSR: empty
+  for (long long tile = warp0; tile < ntiles; tile += nwarps) {
+    const long long pix = tile * PPW + grp;
+    const bool valid = pix < a.npix;
+    unsigned long long beg = 0, end = 0;
+    if (valid) {
+      beg = a.offsets[pix];
+      end = a.offsets[pix + 1];
+      if (end < beg) end = beg;  // malformed CSR: treat as empty (never read out of range)
+    }
     const unsigned long long asb = (beg + off0 + 7u) & ~7ull;
     const unsigned long long ase = (end + off0) & ~7ull;
     unsigned long long hend = end, tbeg = end;
@@ -162,108 +185,117 @@ __global__ void __launch_bounds__(SK_THREADS) sketch_pair_kernel(SketchArgs a) {
       cb = (long long)(asb >> 3);
       ce = (long long)(ase >> 3);
     }
-    uint32_t hA = 0, tA = 0, hB = 0, tB = 0;
-    int since_flush = 0;
-    PairAcc<M> pa;
-    pa.zero();
+    const int nh = (int)(hend - beg), nht = nh + (int)(end - tbeg);  // head/tail peel: < 16 photons
+    // warp-uniform number of chunks
+    int nck = (int)((ce - cb + SO_SLOTS - 1) / SO_SLOTS);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) nck = max(nck, __shfl_xor_sync(0xffffffffu, nck, d));
+    if (nck == 0) nck = 1;
+
     float res[VL];
 #pragma unroll
     for (int i = 0; i < VL; i++) res[i] = 0.f;
+    SortAcc<M> sa;
+    sa.zero();
 
-    auto flush = [&]() {
-      float f[NVP];
+    for (int k = 0; k < nck; k++) {
+      // 1. stage the chunk, partitioned by class (two batches of four 16-byte
+      // loads per lane in flight: register budget of 2 CTAs / SM)
+      const long long s0 = cb + (long long)k * SO_SLOTS + gl;
+      constexpr int QB = SO_SLOTS / SO_G / 2;
+      uint4 v[QB];
 #pragma unroll
-      for (int j = 0; j < M; j++) {
-        f[2 * j] = lo_of(pa.acc[j]);
-        f[2 * j + 1] = hi_of(pa.acc[j]);
+      for (int q = 0; q < QB; q++) {
+        const long long c = s0 + q * SO_G;
+        v[q] = c < ce ? __ldcs(vb + c) : make_uint4(0, 0, 0, 0);
       }
+      __syncwarp();  // the previous chunk's readers are done with qb
+      uint32_t fA = 0, fB = 0;
+      if (k == 0) {  // head/tail peel: up to 4 scalar photons per lane, one partial vector
+        uint32_t hv[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int i = NV; i < NVP; i++) f[i] = 0.f;
-      group_reduce_scatter<NVP, 32>(f, lane);
-#pragma unroll
-      for (int i = 0; i < VL; i++) res[i] += f[i];
-      pa.zero();
-      since_flush = 0;
-    };
-    // one step: lane takes entries (h + lane) and (h + 32 + lane) of each
-    // queue if present (two (A, B) pairs, four chains)
-    auto step = [&](bool useA, bool useB) {
-      const uint32_t ia = hA + (uint32_t)lane, ib = hB + (uint32_t)lane;
-      const uint32_t xa0 = (useA && ia < tA) ? (uint32_t)qA[ia & (PQ_CAP - 1)] : T;
-      const uint32_t xb0 = (useB && ib < tB) ? (uint32_t)qB[ib & (PQ_CAP - 1)] : T;
-      const uint32_t xa1 = (useA && ia + 32u < tA) ? (uint32_t)qA[(ia + 32u) & (PQ_CAP - 1)] : T;
-      const uint32_t xb1 = (useB && ib + 32u < tB) ? (uint32_t)qB[(ib + 32u) & (PQ_CAP - 1)] : T;
-      pa.pair2(tab, xa0, xb0, xa1, xb1, T, j0, invT);
-      if (useA) hA = min(hA + 64u, tA);
-      if (useB) hB = min(hB + 64u, tB);
-      if (++since_flush >= FLUSH_STEPS) flush();
-    };
-
-    // scalar head + tail peel (< 8 photons each): one photon per lane
-    {
-      const int nh = (int)(hend - beg), nt = (int)(end - tbeg);
-      const int nht = nh + nt;
-      if (nht > 0) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        int nv = 0;
-        if (lane < nht) {
-          v.x = bins[lane < nh ? beg + lane : tbeg + (lane - nh)];
-          nv = 1;
+        for (int q = 0; q < 4; q++) {
+          const int idx = gl + q * SO_G;
+          if (idx < nht) hv[q] = bins[idx < nh ? beg + idx : tbeg + (idx - nh)];
         }
-        pq_append(qA, qB, v, nv, T, lane, tA, tB);
-        __syncwarp();
+        const int nq = min(4, max(0, (nht - gl + SO_G - 1) / SO_G));
+        so_append(qb, make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16), 0, 0), (1u << nq) - 1u, T, gl, fA,
+                  fB);
       }
-    }
-    // Main loop with a single call site of the pair body (I-cache): pair
-    // steps while both queues hold a full step, forced single-class steps when
-    // a queue could overflow on the next round, else the next 16-byte round
-    // (32 lanes x 8 photons), and at the end the remainder (absent partners).
-    long long c = cb + lane;
-    uint4 nxt = make_uint4(0, 0, 0, 0);
-    if (c < ce) nxt = __ldcs(vb + c);
-    for (;;) {
-      const uint32_t na = tA - hA, nb = tB - hB;
-      bool useA = true, useB = true;
-      if (na >= 64u && nb >= 64u) {
-      } else if (na > (uint32_t)(PQ_CAP - 256)) {
-        useB = false;
-      } else if (nb > (uint32_t)(PQ_CAP - 256)) {
-        useA = false;
-      } else if (c - lane < ce) {
-        const uint4 v = nxt;
-        const int nv = c < ce ? 8 : 0;
-        if (c + 32 < ce) nxt = __ldcs(vb + c + 32);  // prefetch the lane's next chunk
-        c += 32;
-        __syncwarp();  // earlier steps are done reading the slots being overwritten
-        pq_append(qA, qB, v, nv, T, lane, tA, tB);
-        __syncwarp();
-        continue;
-      } else if (na == 0u && nb == 0u) {
-        break;
-      }
-      step(useA, useB);
-    }
-    flush();
-    const unsigned long long n = end - beg;
-    const float inv = n ? 1.0f / (float)n : 0.0f;
-    float* zrow = a.z + ((size_t)pix * a.mstride + j0) * 2;
 #pragma unroll
-    for (int i = 0; i < VL; i++) {
-      const int idx = lane * VL + i;
-      if (idx < NV) zrow[idx] = res[i] * inv;
+      for (int h = 0; h < 2; h++) {
+        uint4 w[QB];
+#pragma unroll
+        for (int q = 0; q < QB; q++) {
+          w[q] = v[q];
+          const long long c = s0 + (q + QB) * SO_G;
+          if (h == 0) v[q] = c < ce ? __ldcs(vb + c) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < QB; q++) {
+          const long long c = s0 + (q + h * QB) * SO_G;
+          so_append(qb, w[q], c < ce ? 0xffu : 0u, T, gl, fA, fB);
+        }
+      }
+      __syncwarp();
+      // 2. class A (no rotation), two photons per step
+#pragma unroll 1
+      for (uint32_t i = gl; i < fA; i += 2 * SO_G) {
+        const uint32_t x = qb[i];
+        const uint32_t y = i + SO_G < fA ? (uint32_t)qb[i + SO_G] : T;
+        sa.template pair<false>(tab, x, y, T, j0, invT);
+      }
+      // 3. class B in the rotated frame
+      sa.template frame<true>(std::make_integer_sequence<int, M>{});
+#pragma unroll 1
+      for (uint32_t i = gl; i < fB; i += 2 * SO_G) {
+        const uint32_t x = qb[SO_BTOP - i];
+        const uint32_t y = i + SO_G < fB ? (uint32_t)qb[SO_BTOP - SO_G - i] : T;
+        sa.template pair<true>(tab, x, y, T, j0, invT);
+      }
+      sa.template frame<false>(std::make_integer_sequence<int, M>{});
+      // 4. fold every chunk (<= 68 photons per lane per fp32 partial; the
+      // accumulators are dead while the next chunk is staged)
+      {
+        float f[NVP];
+#pragma unroll
+        for (int j = 0; j < M; j++) {
+          f[2 * j] = lo_of(sa.acc[j]);
+          f[2 * j + 1] = hi_of(sa.acc[j]);
+        }
+#pragma unroll
+        for (int i = NV; i < NVP; i++) f[i] = 0.f;
+        group_reduce_scatter<NVP, SO_G>(f, gl);
+#pragma unroll
+        for (int i = 0; i < VL; i++) res[i] += f[i];
+        sa.zero();
+      }
     }
-    __syncwarp();
+    if (valid) {
+      const unsigned long long n = end - beg;
+      const float inv = n ? 1.0f / (float)n : 0.0f;
+      float* zrow = a.z + ((size_t)pix * a.mstride + j0) * 2;
+#pragma unroll
+      for (int i = 0; i < VL; i++) {
+        const int idx = gl * VL + i;
+        if (idx < NV) zrow[idx] = res[i] * inv;
+      }
+    }
   }
 }
 
+size_t sketch_pair_smem(uint32_t T) {
+  return sizeof(float2) * (((size_t)T + 2) & ~(size_t)1) + (size_t)SO_GROUPS * SO_CAP * sizeof(uint16_t);
+}
+
 template <int M>
-static cudaError_t launch_pair_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
-  auto fn = sketch_pair_kernel<M>;
-  const size_t smem = sizeof(float2) * (((size_t)a.T + 2) & ~(size_t)1) + (size_t)(SK_THREADS / 32) * PQ_SMEM_PER_WARP;
+static cudaError_t launch_sorted_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
+  auto fn = sketch_sorted_kernel<M>;
+  const size_t smem = sketch_pair_smem(a.T);
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(SK_MAX_SMEM + 16 + (SK_THREADS / 32) * PQ_SMEM_PER_WARP));
+                                         (int)sketch_pair_smem(SO_MAX_T));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -272,7 +304,9 @@ static cudaError_t launch_pair_t(const SketchArgs& a, cudaStream_t s, int num_sm
   cudaError_t e = occupancy_cached(occ, fn, SK_THREADS, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const long long need = (a.npix + (SK_THREADS / 32) - 1) / (SK_THREADS / 32);
+  constexpr int PPW = 32 / SO_G;
+  const long long tiles = (a.npix + PPW - 1) / PPW;
+  const long long need = (tiles + (SK_THREADS / 32) - 1) / (SK_THREADS / 32);
   long long grid = (long long)per_sm * num_sms;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
@@ -280,15 +314,11 @@ static cudaError_t launch_pair_t(const SketchArgs& a, cudaStream_t s, int num_sm
   return cudaGetLastError();
 }
 
-size_t sketch_pair_smem(uint32_t T) {
-  return sizeof(float2) * (((size_t)T + 2) & ~(size_t)1) + (size_t)(SK_THREADS / 32) * PQ_SMEM_PER_WARP;
-}
-
 cudaError_t launch_sketch_pair(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
   switch (M) {
 #define SRT3D_CASE(MM) \
   case MM:             \
-    return launch_pair_t<MM>(a, s, num_sms);
+    return launch_sorted_t<MM>(a, s, num_sms);
     SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
     SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
     SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)

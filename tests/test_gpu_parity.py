@@ -140,11 +140,13 @@ def test_sketch_lane_regimes_forced(gpu, oracle_mod, inputs_mod):
 
 
 @pytest.mark.parametrize("T,m", [(8192, 32), (8192, 64), (4613, 10), (1024, 4), (2500, 20), (2, 1), (3, 2),
-                                 (17, 16), (24575, 33), (100, 7)])
+                                 (17, 16), (23800, 33), (100, 7)])
 @pytest.mark.parametrize("max_n", [9, 300, 3000])
 def test_sketch_paired_path_parity(gpu, oracle_mod, inputs_mod, T, m, max_n):
-    """Paired path (one warp per pixel, class-sorted Chebyshev pairs) forced on ragged frames with
-    empty pixels, heads/tails of every length and pixels spanning many 256-photon rounds."""
+    """Class-sorted path (PATH_PAIRED: 4 lanes per pixel, photons staged in shared memory by
+    rotation class, class-uniform Chebyshev loops with a frame switch) forced on ragged frames
+    with empty pixels, heads/tails of every length and pixels spanning many 256-photon chunks;
+    T = 23800 is the largest T the path accepts."""
     import torch
 
     bins, offs = inputs_mod.random_csr(npix=333, T=T, max_n=max_n, seed=T * 3 + m + max_n)
@@ -155,11 +157,11 @@ def test_sketch_paired_path_parity(gpu, oracle_mod, inputs_mod, T, m, max_n):
     assert np.all(zg[np.diff(offs.astype(np.int64)) == 0] == 0)
 
 
-@pytest.mark.parametrize("T", [8192, 4613, 24575, 1024])
+@pytest.mark.parametrize("T", [8192, 4613, 23800, 1024])
 def test_sketch_paired_worst_bins(gpu, oracle_mod, T):
     """Every photon of a pixel at one bin (no averaging of phasor errors): the bins where the
     unrotated recurrence is worst conditioned (0, 1, T/2 +- 1, T-1), the class boundaries
-    (4u = T, 3T), and one-class pixels larger than the queue (forced single-class steps)."""
+    (4u = T, 3T), and one-class pixels spanning many chunks."""
     import torch
 
     u = [T // 8, (3 * T) // 8, (T + 7) // 8, T // 4]
@@ -195,7 +197,7 @@ def test_sketch_paired_alignment_and_determinism(gpu, oracle_mod, inputs_mod):
     z2 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED))
     assert np.array_equal(z1.view(np.uint64), z2.view(np.uint64))
     with pytest.raises(gpu.Srt3dError):
-        gpu.srt3d_sketch_ex(db, do, 30000, m, path=gpu.PATH_PAIRED)
+        gpu.srt3d_sketch_ex(db, do, 23801, m, path=gpu.PATH_PAIRED)
 
 
 def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):

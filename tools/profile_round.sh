@@ -13,7 +13,7 @@ ncu --set full --clock-control none --import-source on -k regex:"sketch_kernel|g
 python tools/prof_kernels.py C4 --n 1000000 --iters 0 > $O/pre3.log 2>&1 || exit 1
 ncu --set full --clock-control none -k regex:sketch_hist --launch-count 1 -o $O/c4e6_hist python tools/prof_kernels.py C4 --n 1000000 --iters 0 > $O/ncu_c4.log 2>&1
 ncu --set full --clock-control none -k regex:sketch_hist --launch-count 1 -o $O/c3_hist python tools/prof_kernels.py C3 --iters 0 > $O/ncu_c3.log 2>&1
-ncu --set full --clock-control none -k regex:"scatter_kernel|count_kernel" --launch-count 2 -o $O/bucket_full python tools/bucket_probe.py > $O/ncu_bk.log 2>&1
+ncu --set full --clock-control none -k regex:"coarse_count|partition_kernel|bucket_fine" --launch-count 3 -o $O/bucket_full python tools/bucket_probe.py > $O/ncu_bk.log 2>&1
 ls $O/*.ncu-rep
 # summaries (the .ncu-rep files are too large to bring back together)
 python tools/launch_summary.py $O/launches_c5.csv $O/r01_launches_c5.json > /dev/null
