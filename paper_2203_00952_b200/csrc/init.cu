@@ -16,6 +16,7 @@
 // memory once per 4 points).  The greedy picking reads the warp's g row from
 // shared memory; K rounds of a warp-wide argmax over the candidates.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -266,6 +267,13 @@ size_t backproject_smem(uint32_t N, bool pick) {
 
 cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int num_sms) {
   if (a.npix <= 0) return cudaSuccess;
+  // tensor-core path where the shape allows it (SRT3D_INIT_CUDA_CORES=1 forces
+  // this kernel: A/B timing and parity of both paths)
+  static const bool force_cores = [] {
+    const char* e = getenv("SRT3D_INIT_CUDA_CORES");
+    return e && e[0] == '1';
+  }();
+  if (!force_cores && backproject_tc_supported(a.N, a.m)) return launch_backproject_tc(a, pick, s, num_sms);
   const size_t smem = backproject_smem(a.N, pick);
   auto fn = pick ? backproject_kernel<true> : backproject_kernel<false>;
   static bool attr_set[2] = {false, false};  // benign race: idempotent

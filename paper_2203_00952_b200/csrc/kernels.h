@@ -116,6 +116,9 @@ struct BpArgs {
   float hh[MAX_M];  // hhat_l
 };
 cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int num_sms);
+// tensor-core backprojection (init_tc.cu): N % 32 == 0, 32 <= N <= 512, m <= 32
+bool backproject_tc_supported(uint32_t N, uint32_t m);
+cudaError_t launch_backproject_tc(const BpArgs& a, bool pick, cudaStream_t s, int num_sms);
 cudaError_t launch_init_k1(const BpArgs& a, cudaStream_t s);
 size_t backproject_smem(uint32_t N, bool pick);
 // NEXT-4 streaming acquisition (stream.cu).

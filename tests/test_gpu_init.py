@@ -38,7 +38,10 @@ def _gpu_sketch(gpu, bins, offs, T, m):
 
 @pytest.mark.parametrize("T,m,N,sigma", [(1024, 4, 1024, 2.0), (4613, 10, 300, 5.0), (2500, 20, 129, 3.0),
                                          (8192, 32, 8192, 6.0), (8192, 64, 1000, 0.0), (100, 1, 7, 0.0),
-                                         (17, 16, 1, 1.0), (4096, 10, 4096, 4.0)])
+                                         (17, 16, 1, 1.0), (4096, 10, 4096, 4.0),
+                                         # tensor-core path (N % 32 == 0, N <= 512, m <= 32)
+                                         (8192, 32, 512, 6.0), (4613, 10, 256, 5.0), (2500, 20, 32, 3.0),
+                                         (1024, 1, 64, 2.0), (8192, 31, 480, 6.0), (4096, 17, 96, 0.0)])
 def test_backproject_parity(gpu, oracle_mod, inputs_mod, T, m, N, sigma):
     import torch
 
@@ -51,6 +54,31 @@ def test_backproject_parity(gpu, oracle_mod, inputs_mod, T, m, N, sigma):
     S = np.sum(_hh(sigma, T, m) * np.abs(zh), axis=1)[:, None]
     d = np.abs(g.cpu().numpy() - go)
     assert np.all(d <= 1e-5 * S + 1e-30), float((d / (S + 1e-30)).max())
+
+
+def test_backproject_tc_many_tiles(gpu, oracle_mod, inputs_mod):
+    """Tensor-core path over many 128-pixel tiles per persistent CTA (and a partial last tile):
+    sampled rows against the oracle, plus init_depths picks on the same rows."""
+    import torch
+
+    T, m, N, sigma = 8192, 32, 512, 6.0
+    npix = 148 * 128 * 2 + 77
+    bins, offs = inputs_mod.random_csr(npix=npix, T=T, max_n=60, seed=5)
+    z = _gpu_sketch(gpu, bins, offs, T, m)
+    g = gpu.srt3d_backproject(z, sigma, T, N)
+    tg, gg, ag, cg = gpu.srt3d_init_depths(z, sigma, T, N, 3, 50)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([[0, 127, 128, npix - 1], rng.choice(npix, 600, replace=False)]))
+    zh = z.cpu().numpy()[idx]
+    go = oracle_mod.backproject(zh, sigma, T, N)
+    S = np.sum(_hh(sigma, T, m) * np.abs(zh), axis=1)[:, None]
+    d = np.abs(g.cpu().numpy()[idx] - go)
+    assert np.all(d <= 1e-5 * S + 1e-30), float((d / (S + 1e-30)).max())
+    to, _, _, co = oracle_mod.init_depths(go, sigma, T, m, 3, 50)
+    tgh, cgh = tg.cpu().numpy()[idx], cg.cpu().numpy()[idx]
+    bad = _check_picks(tgh, cgh, 2e-5 * S[:, 0], to.astype(np.float32), co, lambda i: go[i], T, N, 50)
+    assert bad <= len(idx) // 20, bad
 
 
 def _check_picks(tg, cg, tol_g, to, co, go_row_fn, T, N, min_sep):
