@@ -24,13 +24,17 @@
 //    2 halves x 2 K-columns x 4 k-steps x 3 products = 48 tcgen05.mma
 //    (kind::tf32, M = 128, N = N/2, K = 8) into a TMEM accumulator of N fp32
 //    columns (lane = pixel), committed to an mbarrier.
-//  * Epilogue: thread = pixel = TMEM lane; tcgen05.ld 32 columns at a time.
-//    Backprojection writes the row; init_depths finds the candidates (g_n > 0,
-//    g_n > g_{n-1}, g_n >= g_{n+1}, circular) and the first pick in one pass
-//    (candidate bit masks kept in shared memory), then each further pick
-//    re-reads the accumulator with the exclusion zones of the earlier picks as
-//    per-chunk bit masks — the oracle's rule and tie order (largest g, then
-//    smallest n).
+//  * Epilogue: 16 warps; warp w reads TMEM lanes 32 (w % 4) .. (its pixels)
+//    and the grid columns of split w / 4 (a quarter of the N columns), 32
+//    columns per tcgen05.ld.  Backprojection stages each 32 x 32 block through
+//    shared memory for row-contiguous stores; init_depths finds its split's
+//    candidates (g_n > 0, g_n > g_{n-1}, g_n >= g_{n+1}, circular; the split's
+//    boundary neighbours read from the adjacent chunks) and local best in one
+//    pass (candidate bit masks in shared memory, tree argmax per chunk), the
+//    four splits' bests are combined through shared memory, and each further
+//    pick re-reads the split's columns with the exclusion zones of the earlier
+//    picks as per-chunk bit masks — the oracle's rule and tie order (largest
+//    g, then smallest n).
 // Supported: N % 32 == 0, 32 <= N <= 512, m <= 32; other shapes use the CUDA-
 // core kernel (init.cu).
 #include <cstdint>
@@ -42,8 +46,9 @@ namespace srt3d {
 
 namespace {
 
-constexpr int TC_THREADS = 128;
 constexpr int TC_M = 128;          // pixels per tile (TMEM lanes)
+constexpr int TC_SPLIT = 4;        // column splits of the epilogue: 4 warps per TMEM lane quarter
+constexpr int TC_THREADS = TC_M * TC_SPLIT;
 constexpr uint32_t A_CHUNK = TC_M * 128;  // one 128-byte swizzle column of A: 16 KB
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -122,6 +127,31 @@ __device__ __forceinline__ uint32_t excl_bits(int p, int D, int N, int c0) {
   return b;
 }
 
+// max of 32 values and its index (ties: the smaller index), as a tree: the
+// epilogue runs one warp per SM sub-partition, so a serial max chain would be
+// latency-bound
+__device__ __forceinline__ void tree_argmax32(const float (&x)[32], float& mx, int& im) {
+  float y[16];
+  int iy[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const bool t = x[2 * k + 1] > x[2 * k];
+    y[k] = t ? x[2 * k + 1] : x[2 * k];
+    iy[k] = t ? 2 * k + 1 : 2 * k;
+  }
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int k = 0; k < w; k++) {
+      const bool t = y[2 * k + 1] > y[2 * k];
+      y[k] = t ? y[2 * k + 1] : y[2 * k];
+      iy[k] = t ? iy[2 * k + 1] : iy[2 * k];
+    }
+  }
+  mx = y[0];
+  im = iy[0];
+}
+
 template <bool PICK>
 __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
   extern __shared__ unsigned char tc_raw[];
@@ -132,10 +162,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
   unsigned char* a_lo = a_hi + 2 * A_CHUNK;
   unsigned char* b_hi = a_lo + 2 * A_CHUNK;          // 2 K columns x NH rows x 128 B
   unsigned char* b_lo = b_hi + 2 * NH * 128;
-  uint32_t* cand_all = reinterpret_cast<uint32_t*>(b_lo + 2 * NH * 128);  // [NC][TC_THREADS] (PICK)
+  uint32_t* cand_all = reinterpret_cast<uint32_t*>(b_lo + 2 * NH * 128);  // [NC][TC_M] (PICK)
   __shared__ __align__(8) uint64_t mma_bar;
   __shared__ uint32_t tmem_slot;
+  __shared__ float xb_v[2][TC_SPLIT][TC_M];  // per-round local bests of the column splits
+  __shared__ int xb_i[2][TC_SPLIT][TC_M];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, split = warp >> 2;  // TMEM lanes 32*quarter.. ; column split
+  const int prow = quarter * 32 + lane;             // pixel row within the tile = TMEM lane
+  // this thread's 32-column chunks [c0, c1) of the grid
+  const int c0 = split * NC / TC_SPLIT, c1 = (split + 1) * NC / TC_SPLIT;
 
   // ---- one-time setup: B (hi, lo) for the first half grid, barrier, TMEM ----
   for (int e = tid; e < NH * 32; e += TC_THREADS) {
@@ -185,13 +221,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
   const long long ntiles = (a.npix + TC_M - 1) / TC_M;
   uint32_t phase = 0;
 
-  // the z rows of a tile: warp w holds rows 32w .. 32w+31, lane = frequency l - 1
+  // the z rows of a tile: warp w holds rows RPW*w .. , lane = frequency l - 1
   // (loads for tile t+1 are issued at the start of tile t's epilogue)
-  float2 zpre[TC_M / 4];
+  constexpr int RPW = TC_M / (TC_THREADS / 32);
+  float2 zpre[RPW];
   auto load_tile = [&](long long t) {
-    const long long r0 = t * TC_M + warp * (TC_M / 4);
+    const long long r0 = t * TC_M + warp * RPW;
 #pragma unroll
-    for (int rr = 0; rr < TC_M / 4; rr++) {
+    for (int rr = 0; rr < RPW; rr++) {
       const long long pix = r0 + rr;
       zpre[rr] = (t < ntiles && pix < a.npix && (uint32_t)lane < m) ? zg[(size_t)pix * m + lane] : make_float2(0.f, 0.f);
     }
@@ -204,8 +241,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
     {
       const uint32_t i = (uint32_t)lane >> 1, col = (lane & 1) ? 0u : 1u;  // frequency l = lane + 1
 #pragma unroll
-      for (int rr = 0; rr < TC_M / 4; rr++) {
-        const uint32_t r = (uint32_t)(warp * (TC_M / 4) + rr);
+      for (int rr = 0; rr < RPW; rr++) {
+        const uint32_t r = (uint32_t)(warp * RPW + rr);
         const float2 v = zpre[rr];
         const float hx = __uint_as_float(tf32_rna(v.x)), hy = __uint_as_float(tf32_rna(v.y));
         const float lx = __uint_as_float(tf32_rna(v.x - hx)), ly = __uint_as_float(tf32_rna(v.y - hy));
@@ -245,124 +282,160 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    // ---- epilogue: thread = pixel = TMEM lane ----
+    // ---- epilogue: (pixel = TMEM lane) x (column split) per thread ----
     load_tile(tile + gridDim.x);  // next tile's z in flight during the epilogue
-    const long long pix = row0 + tid;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const long long pix = row0 + prow;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     float v[32];
     if (!PICK) {
-      // per 32-column chunk: rows through shared memory (the A buffer is free
-      // until the next tile) so each warp store covers whole 128-byte row runs
-      float* stg = reinterpret_cast<float*>(a_hi) + warp * 32 * 36;  // 32 rows, stride 36 floats
-      for (int c = 0; c < NC; c++) {
+      // per 32-column chunk: the warp's 32 rows through shared memory (the A
+      // buffers are free until the next tile; float4 slots XOR-swizzled) so
+      // each warp store covers whole 128-byte row runs
+      float* stg = reinterpret_cast<float*>(a_hi) + warp * 32 * 32;
+      for (int c = c0; c < c1; c++) {
         tmem_ld32(trow + (uint32_t)(c * 32), v);
 #pragma unroll
         for (int q = 0; q < 8; q++)
-          *reinterpret_cast<float4*>(stg + lane * 36 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          *reinterpret_cast<float4*>(stg + lane * 32 + 4 * (q ^ (lane & 7))) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 8; q++) {  // 4 rows x 128 B per warp store
           const int r = q * 4 + (lane >> 3), c4 = lane & 7;
-          const long long pr = row0 + warp * 32 + r;
+          const long long pr = row0 + quarter * 32 + r;
           if (pr < a.npix)
             *reinterpret_cast<float4*>(a.g + (size_t)pr * N + c * 32 + 4 * c4) =
-                *reinterpret_cast<const float4*>(stg + r * 36 + 4 * c4);
+                *reinterpret_cast<const float4*>(stg + r * 32 + 4 * (c4 ^ (r & 7)));
         }
         __syncwarp();
       }
     } else {
-      uint32_t* cand = cand_all + tid;  // cand[c * TC_THREADS]
-      // round 0: candidate masks and the first pick
-      tmem_ld32(trow + (uint32_t)(N - 32), v);
-      float prevv = v[31], first = 0.f, pend = 0.f, pendp = 0.f;
+      uint32_t* cand = cand_all + prow;  // cand[c * TC_M]
+      // round 0 over this split's chunks: candidate masks and the local best
       float best = 0.f;
       int bn = -1;
-      for (int c = 0; c < NC; c++) {
-        tmem_ld32(trow + (uint32_t)(c * 32), v);
-        if (c == 0) {
-          first = v[0];
-        } else {  // element 31 of chunk c-1 (its right neighbour is v[0])
-          const bool ok = pend > 0.f && pend > pendp && pend >= v[0];
-          if (ok) cand[(c - 1) * TC_THREADS] |= 1u << 31;
-          if (ok && pend > best) {
-            best = pend;
-            bn = (c - 1) * 32 + 31;
+      if (c1 > c0) {
+        tmem_ld32(trow + (uint32_t)(((c0 + NC - 1) % NC) * 32), v);
+        float prevv = v[31];  // g[32 c0 - 1] (circular)
+        tmem_ld32(trow + (uint32_t)((c1 % NC) * 32), v);
+        const float nextv = v[0];  // g[32 c1] (circular)
+        float pend = 0.f, pendp = 0.f;
+        for (int c = c0; c < c1; c++) {
+          tmem_ld32(trow + (uint32_t)(c * 32), v);
+          if (c > c0) {  // element 31 of chunk c-1 (its right neighbour is v[0])
+            const bool ok = pend > 0.f && pend > pendp && pend >= v[0];
+            if (ok) cand[(c - 1) * TC_M] |= 1u << 31;
+            if (ok && pend > best) {
+              best = pend;
+              bn = (c - 1) * 32 + 31;
+            }
           }
-        }
-        uint32_t bits = 0u;
+          uint32_t bits = 0u;
+          float x[32];
 #pragma unroll
-        for (int i = 0; i < 31; i++) {
-          const float g = v[i], gp = i == 0 ? prevv : v[i - 1];
-          const bool ok = g > 0.f && g > gp && g >= v[i + 1];
-          bits |= ok ? (1u << i) : 0u;
-          if (ok && g > best) {
-            best = g;
-            bn = c * 32 + i;
+          for (int i = 0; i < 31; i++) {
+            const float g = v[i], gp = i == 0 ? prevv : v[i - 1];
+            const bool ok = g > 0.f && g > gp && g >= v[i + 1];
+            bits |= ok ? (1u << i) : 0u;
+            x[i] = ok ? g : 0.f;  // candidates are > 0
           }
+          x[31] = 0.f;
+          float cm;
+          int ci;
+          tree_argmax32(x, cm, ci);
+          if (cm > best) {
+            best = cm;
+            bn = c * 32 + ci;
+          }
+          cand[c * TC_M] = bits;
+          pend = v[31];
+          pendp = v[30];
+          prevv = v[31];
         }
-        cand[c * TC_THREADS] = bits;
-        pend = v[31];
-        pendp = v[30];
-        prevv = v[31];
-      }
-      {  // n = N - 1 (right neighbour: n = 0)
-        const bool ok = pend > 0.f && pend > pendp && pend >= first;
-        if (ok) cand[(NC - 1) * TC_THREADS] |= 1u << 31;
+        const bool ok = pend > 0.f && pend > pendp && pend >= nextv;  // n = 32 c1 - 1
+        if (ok) cand[(c1 - 1) * TC_M] |= 1u << 31;
         if (ok && pend > best) {
           best = pend;
-          bn = N - 1;
+          bn = c1 * 32 - 1;
         }
       }
+      // K rounds: combine the splits' local bests (largest g, then smallest n);
+      // every split thread of a pixel keeps the same pick list
       int pick[MAX_K];
       float pg[MAX_K];
       int cnt = 0;
-      if (bn >= 0) {
-        pick[0] = bn;
-        pg[0] = best;
-        cnt = 1;
-      }
-      // further picks: re-read the accumulator, candidates outside every exclusion zone
-      for (uint32_t k = 1; k < a.K; k++) {
-        const bool live = cnt == (int)k;
-        if (!__any_sync(0xffffffffu, live)) break;
-        best = 0.f;
-        bn = -1;
-        for (int c = 0; c < NC; c++) {
-          uint32_t elig = 0u;
-          if (live) {
-            elig = cand[c * TC_THREADS];
-            for (int q = 0; q < cnt; q++) elig &= ~excl_bits(pick[q], D, N, c * 32);
-          }
-          if (!__any_sync(0xffffffffu, elig != 0u)) continue;
-          tmem_ld32(trow + (uint32_t)(c * 32), v);
+      for (uint32_t k = 0; k < a.K; k++) {
+        const int buf = k & 1;
+        if (k > 0) {  // local best outside the exclusion zones of the picks so far
+          best = 0.f;
+          bn = -1;
+          const bool live = cnt == (int)k;
+          for (int c = c0; c < c1; c++) {
+            uint32_t elig = 0u;
+            if (live) {
+              elig = cand[c * TC_M];
 #pragma unroll
-          for (int i = 0; i < 32; i++) {
-            if (((elig >> i) & 1u) && v[i] > best) {
-              best = v[i];
-              bn = c * 32 + i;
+              for (int q = 0; q < MAX_K; q++)
+                if (q < cnt) elig &= ~excl_bits(pick[q], D, N, c * 32);
+            }
+            if (!__any_sync(0xffffffffu, elig != 0u)) continue;
+            tmem_ld32(trow + (uint32_t)(c * 32), v);
+            float x[32];
+#pragma unroll
+            for (int i = 0; i < 32; i++) x[i] = ((elig >> i) & 1u) ? v[i] : 0.f;
+            float cm;
+            int ci;
+            tree_argmax32(x, cm, ci);
+            if (cm > best) {
+              best = cm;
+              bn = c * 32 + ci;
             }
           }
         }
-        if (live && bn >= 0) {
-          pick[cnt] = bn;
-          pg[cnt] = best;
+        xb_v[buf][split][prow] = best;
+        xb_i[buf][split][prow] = bn;
+        __syncthreads();
+        float gb = 0.f;
+        int gi = -1;
+#pragma unroll
+        for (int q = 0; q < TC_SPLIT; q++) {  // splits cover increasing n: strict > keeps the smaller n
+          const int qi = xb_i[buf][q][prow];
+          const float qv = xb_v[buf][q][prow];
+          if (qi >= 0 && (gi < 0 || qv > gb)) {
+            gb = qv;
+            gi = qi;
+          }
+        }
+        if (cnt == (int)k && gi >= 0) {
+#pragma unroll
+          for (int q = 0; q < MAX_K; q++)
+            if (q == cnt) {
+              pick[q] = gi;
+              pg[q] = gb;
+            }
           cnt++;
         }
       }
-      if (pix < a.npix) {
-        for (int x = 1; x < cnt; x++)  // sort by depth
-          for (int y = x; y > 0 && pick[y - 1] > pick[y]; y--) {
-            const int tp = pick[y];
-            pick[y] = pick[y - 1];
-            pick[y - 1] = tp;
-            const float tg = pg[y];
-            pg[y] = pg[y - 1];
-            pg[y - 1] = tg;
-          }
+      if (split == 0 && pix < a.npix) {
+        // sort by depth (insertion sort on the register arrays: compile-time indices)
+#pragma unroll
+        for (int x = 1; x < MAX_K; x++)
+#pragma unroll
+          for (int y = x; y > 0; y--)
+            if (y < cnt && pick[y - 1] > pick[y]) {
+              const int tp = pick[y];
+              pick[y] = pick[y - 1];
+              pick[y - 1] = tp;
+              const float tg = pg[y];
+              pg[y] = pg[y - 1];
+              pg[y - 1] = tg;
+            }
         const double tfirst = cnt ? (double)pick[0] * (double)a.T / (double)N : 0.0;
-        for (uint32_t k = 0; k < a.K; k++) {
+#pragma unroll
+        for (int k = 0; k < MAX_K; k++) {
+          if (k >= (int)a.K) break;
           const size_t o = (size_t)pix * a.K + k;
-          if ((int)k < cnt) {
+          if (k < cnt) {
             a.t_out[o] = (float)((double)pick[k] * (double)a.T / (double)N);
             a.g_out[o] = pg[k];
             a.a_out[o] = fminf(fmaxf(pg[k] * a.inv_sh2, 0.f), 1.f);
@@ -385,7 +458,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
 
 size_t bp_tc_smem(uint32_t N, bool pick) {
   const size_t nh = N / 2;
-  return 1024 + 4 * (size_t)A_CHUNK + 2 * 2 * nh * 128 + (pick ? sizeof(uint32_t) * (N / 32) * TC_THREADS : 0);
+  return 1024 + 4 * (size_t)A_CHUNK + 2 * 2 * nh * 128 + (pick ? sizeof(uint32_t) * (N / 32) * TC_M : 0);
 }
 
 }  // namespace
