@@ -482,10 +482,29 @@ def run_srt3d(args):
         d_f = f.npix * 8.0 * f.m * init_ms["N"]
         k_b = f.npix * (8.0 * f.m + 8.0)
         k_f = f.npix * 8.0 * f.m
+        n_grid = init_ms["N"]
+        tc_path = n_grid % 32 == 0 and 32 <= n_grid <= 512 and f.m <= 32  # init_tc.cu shapes
+        if tc_path:
+            # tensor-core path: the backprojection is the GEMM [Re z, Im z] (npix x 2m) x B^T (2m x N);
+            # algorithmic flops 2 (2m) N per pixel (the hi/lo split executes 3x that); TF32 dense peak =
+            # the measured bf16 peak x 1.1/2.25 (B200_PROFILING.md nominal ratio)
+            bf16 = float(peaks.get("bf16_tflops", 1653.6)) * 1e12
+            tf32_peak = bf16 * 1.1 / 2.25
+            t_alg = f.npix * 2.0 * (2.0 * f.m) * n_grid
+            t_run = init_ms["depths_ms"] * 1e-3
+            d_roof = {"kernel": "srt3d_init_depths", "bound": "tensor", "achieved": t_alg / t_run / 1e12,
+                      "peak": tf32_peak / 1e12, "unit": "TFLOP/s", "frac": t_alg / tf32_peak / t_run,
+                      "peak_source": "MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (TF32 dense)",
+                      "alg_flops_per_launch": t_alg, "executed_tensor_flops_per_launch": 3.0 * f.npix * 2.0 * 64 * n_grid,
+                      "note": "tcgen05 kind::tf32 (3-term split) + pick epilogue; the epilogue (candidate scan and K "
+                              "rounds over the TMEM accumulator) bounds the kernel, the MMAs are ~14% of it (ncu)"}
+        else:
+            d_roof = roofline("srt3d_init_depths", d_b, d_f, init_ms["depths_ms"])
         init = {"init_depths": {"kernel": "srt3d_init_depths", "grid_N": init_ms["N"], "K": init_ms["K"],
                                 "min_sep": init_ms["min_sep"], "ms": init_ms["depths_ms"],
+                                "path": "tensor cores (tcgen05)" if tc_path else "cuda cores",
                                 "pixels_per_s": f.npix / (init_ms["depths_ms"] * 1e-3),
-                                "roofline": roofline("srt3d_init_depths", d_b, d_f, init_ms["depths_ms"])},
+                                "roofline": d_roof},
                 "init_k1": {"kernel": "srt3d_init_k1", "ms": init_ms["k1_ms"],
                             "pixels_per_s": f.npix / (init_ms["k1_ms"] * 1e-3),
                             "roofline": roofline("srt3d_init_k1", k_b, k_f, init_ms["k1_ms"])},
