@@ -198,6 +198,10 @@ int srt3d_fit_pixelwise(const float* z, float* t, float* alpha, int64_t npix, ui
  * t_n = n*T/N, n = 0..N-1 (a circular grid), hhat Gaussian with sigma.
  *   z  float [npix][m][2] (8-byte aligned); g float [npix][N] output.
  *   1 <= N <= 8192.  Errors as srt3d_expected_sketch; N out of range: EINVAL.
+ *   N % 32 == 0, N <= 512, m <= 32: computed on the tensor cores (tcgen05
+ *   TF32 with a hi/lo split: fp32-level accuracy; the
+ *   environment variable SRT3D_INIT_CUDA_CORES=1, read once per process,
+ *   forces the CUDA-core kernel); other shapes on the CUDA cores.
  */
 int srt3d_backproject(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, uint32_t N, float* g,
                       void* stream);
@@ -210,7 +214,8 @@ int srt3d_backproject(const float* z, int64_t npix, float sigma, uint32_t T, uin
  * by depth: t [npix][K] = n*T/N, g_at [npix][K], alpha [npix][K] =
  * clamp(g_at / sum_l hhat_l^2, 0, 1), count [npix] (int32) = picks made.
  * Unfilled slots (reading A14): t = (t_first + T/2) mod T, g_at = alpha = 0.
- *   3 <= N <= 4096, 1 <= K <= SRT3D_MAX_K, min_sep in bins.
+ *   3 <= N <= 4096, 1 <= K <= SRT3D_MAX_K, min_sep in bins.  g as
+ *   srt3d_backproject (tensor cores for N % 32 == 0, N <= 512, m <= 32).
  */
 int srt3d_init_depths(const float* z, int64_t npix, float sigma, uint32_t T, uint32_t m, uint32_t N, uint32_t K,
                       uint32_t min_sep, float* t, float* g_at, float* alpha, int32_t* count, void* stream);
