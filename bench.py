@@ -56,7 +56,10 @@ def parse():
     ap.add_argument("--init-grid", type=int, default=0, help="backprojection grid points (default 16 m)")
     ap.add_argument("--init-min-sep", type=int, default=50, help="minimum separation of initial depths (bins)")
     ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 bucketing / merge timings")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
+    return args
 
 
 def load_peaks():
@@ -528,7 +531,7 @@ def run_srt3d(args):
         stream = {"bucket_events": {"kernel": "srt3d_bucket_events", "events": f.n_photons, "ms": stream_ms["bucket_ms"],
                                     "events_per_s": f.n_photons / (stream_ms["bucket_ms"] * 1e-3),
                                     "roofline": roofline("srt3d_bucket_events", b_b, 0.0, stream_ms["bucket_ms"]),
-                                    "note": "count + scan + scatter; pixel ids read twice, 2 global atomics per event"},
+                                    "note": "two-level counting sort (coarse histogram, bucket partition, per-bucket tile sort); algorithmic 8 B/event (read 6, write 2), design traffic 24 B/event (DESIGN.md §5.6)"},
                   "sketch_merge": {"kernel": "srt3d_sketch_merge", "ms": stream_ms["merge_ms"],
                                    "roofline": roofline("srt3d_sketch_merge", m_b, 0.0, stream_ms["merge_ms"])},
                   "note": "NEXT-4, timed outside the step"}

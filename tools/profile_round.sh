@@ -8,8 +8,8 @@ python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-init --no-s
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-init --no-stream > $O/ncu_launch.log 2>&1
 python tools/prof_kernels.py C5 --iters 3 --next > $O/pre2.log 2>&1 || exit 1
-ncu --set full --clock-control none --import-source on -k regex:"sketch_kernel|grad_kernel|fit_kernel|backproject|init_k1|merge_kernel" \
-    --launch-skip 0 --launch-count 8 -o $O/c5_full python tools/prof_kernels.py C5 --iters 1 --next > $O/ncu_c5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"sketch_kernel|grad_kernel|fit_kernel|backproject|bp_tc_kernel|init_k1|merge_kernel" \
+    --launch-skip 0 --launch-count 10 -o $O/c5_full python tools/prof_kernels.py C5 --iters 1 --next > $O/ncu_c5.log 2>&1
 python tools/prof_kernels.py C4 --n 1000000 --iters 0 > $O/pre3.log 2>&1 || exit 1
 ncu --set full --clock-control none -k regex:sketch_hist --launch-count 1 -o $O/c4e6_hist python tools/prof_kernels.py C4 --n 1000000 --iters 0 > $O/ncu_c4.log 2>&1
 ncu --set full --clock-control none -k regex:sketch_hist --launch-count 1 -o $O/c3_hist python tools/prof_kernels.py C3 --iters 0 > $O/ncu_c3.log 2>&1
