@@ -41,7 +41,9 @@ def _gpu_sketch(gpu, bins, offs, T, m):
                                          (17, 16, 1, 1.0), (4096, 10, 4096, 4.0),
                                          # tensor-core path (N % 32 == 0, N <= 512, m <= 32)
                                          (8192, 32, 512, 6.0), (4613, 10, 256, 5.0), (2500, 20, 32, 3.0),
-                                         (1024, 1, 64, 2.0), (8192, 31, 480, 6.0), (4096, 17, 96, 0.0)])
+                                         (1024, 1, 64, 2.0), (8192, 31, 480, 6.0), (4096, 17, 96, 0.0),
+                                         # m > 32 at a tensor-core N: routed to the CUDA-core kernel
+                                         (8192, 64, 512, 6.0)])
 def test_backproject_parity(gpu, oracle_mod, inputs_mod, T, m, N, sigma):
     import torch
 
