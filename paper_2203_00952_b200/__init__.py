@@ -80,9 +80,9 @@ def load_library(path: str | None = None):
     lib.srt3d_sketch_accumulate.argtypes = [P, P, P, P, i64, u32, P]
     lib.srt3d_debug_ffma_peak.argtypes = [P]
     lib.srt3d_bucket_scratch_words.argtypes = [i64, u64]
-    lib.srt3d_bucket_scratch_words.restype = u64
     for f in EXPORTS[2:]:
         getattr(lib, f).restype = ctypes.c_int
+    lib.srt3d_bucket_scratch_words.restype = u64  # size_t, not a status code
     if path is None:
         _lib = lib
     return lib
