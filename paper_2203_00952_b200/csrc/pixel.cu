@@ -218,7 +218,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
     }
     // packed: R = z_j - hh Sk ; L2 += R*R ; RHO = hh R ; SIG = (wh, -wh) * R
     const u64 R = ffma2(pk(-hh, -hh), Sk, pk(zj.x, zj.y));
-    L2 = ffma2(R, R, L2);
+    if (MODE != PX_GRAD_STEP_NL) L2 = ffma2(R, R, L2);  // the loss only when it is stored
     const u64 RHO = fmul2(pk(hh, hh), R);   // hhat_j r_j
     const u64 SIG = fmul2(pk(wh, -wh), R);  // omega_j hhat_j (r_r, -r_i)
 #pragma unroll
@@ -240,7 +240,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
 template <int K, int MODE>
 __device__ __forceinline__ void pixel_store(const PixArgs& a, long long i, const float (&tk)[K], const float (&ak)[K],
                                             const float (&gt)[K], const float (&ga)[K], float L) {
-  if (a.loss) a.loss[i] = L;
+  if (MODE != PX_GRAD_STEP_NL && a.loss) a.loss[i] = L;
   if (MODE == PX_GRAD) {
 #pragma unroll
     for (int k = 0; k < K; k++) {
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(GRAD_THREADS) fit_kernel(const PixArgs a, int 
   __syncwarp();
   float gt[K], ga[K], L = 0.f;
   for (int it = 0; it < iters; it++) {
-    pixel_body<K, M, PX_GRAD_STEP, false>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
+    pixel_body<K, M, PX_GRAD_STEP_NL, false>(a, tile + lane * S, s_hh, s_wh, tk, ak, gt, ga, L);
 #pragma unroll
     for (int k = 0; k < K; k++) {
       float tn, an;
@@ -623,8 +623,10 @@ cudaError_t launch_pixel(PixMode mode, int K, const PixArgs& a, cudaStream_t s) 
       return launch_px_k<PX_EXPECTED>(K, a, s);
     case PX_GRAD:
       return launch_px_k<PX_GRAD>(K, a, s);
-    case PX_GRAD_STEP:
-      return launch_px_k<PX_GRAD_STEP>(K, a, s);
+    case PX_GRAD_STEP:  // without a loss output the per-frequency |r|^2 accumulation is compiled out
+      return a.loss ? launch_px_k<PX_GRAD_STEP>(K, a, s) : launch_px_k<PX_GRAD_STEP_NL>(K, a, s);
+    case PX_GRAD_STEP_NL:
+      return launch_px_k<PX_GRAD_STEP_NL>(K, a, s);
     case PX_UPDATE:
       return launch_px_k<PX_UPDATE>(K, a, s);
   }
