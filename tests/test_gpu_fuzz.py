@@ -1,0 +1,90 @@
+"""Seeded randomized GPU <-> oracle parity over the shape space (every path of
+the C ABI on random T, m, K, sigma, frame sizes and photon-count mixes).
+
+Each case draws its own shape from a counter-seeded generator, so a failure
+names a reproducible case id.  Tolerances as tests/test_gpu_parity.py
+(DESIGN.md §6): sketch |delta| <= 1e-5 absolute; loss / gradients per the A12
+per-component bound; backprojection |delta| <= 1e-5 * sum_l hhat_l |z_l|.
+"""
+import numpy as np
+import pytest
+
+from test_gpu_parity import _assert_sketch_close, _dev, _grad_tol_check, _host
+
+pytestmark = pytest.mark.gpu
+
+N_CASES = 64
+
+
+def _case(i):
+    rng = np.random.default_rng(1_000_003 * (i + 1))
+    T = int(rng.choice([2, 3, 17, 100, 1000, 2500, 4096, 4613, 8192, 12000, 23800, 30000, 65535]))
+    m = int(rng.integers(1, min(64, T - 1) + 1)) if T > 2 else 1
+    npix = int(rng.choice([1, 7, 129, 1000, 3001]))
+    max_n = int(rng.choice([0, 1, 9, 100, 700, 4000]))
+    K = int(rng.integers(1, 9))
+    sigma = float(rng.choice([0.0, 0.5, 2.0, 6.0]))
+    return dict(T=T, m=m, npix=npix, max_n=max_n, K=K, sigma=sigma, seed=int(rng.integers(1 << 30)))
+
+
+@pytest.mark.parametrize("i", range(N_CASES))
+def test_fuzz_sketch_paths(gpu, oracle_mod, inputs_mod, i):
+    """Every sketch regime the shape admits (auto, direct at 4/8/16/32 lanes, bin-count, class-sorted)
+    against the oracle, on a random ragged frame."""
+    import torch
+
+    c = _case(i)
+    T, m = c["T"], c["m"]
+    bins, offs = inputs_mod.random_csr(npix=c["npix"], T=T, max_n=c["max_n"], seed=c["seed"])
+    zo = oracle_mod.sketch(bins, offs, T, m)
+    db = _dev(bins) if bins.size else torch.zeros(1, dtype=torch.uint16, device="cuda")
+    do = _dev(offs)
+    regimes = [(gpu.PATH_AUTO, 0), (gpu.PATH_DIRECT, 4), (gpu.PATH_DIRECT, 8), (gpu.PATH_DIRECT, 16),
+               (gpu.PATH_DIRECT, 32)]
+    if T <= 16384:
+        regimes.append((gpu.PATH_BINCOUNT, 0))
+    if T <= 23800:
+        regimes.append((gpu.PATH_PAIRED, 0))
+    for path, lanes in regimes:
+        try:
+            z = gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=path, lanes_per_pixel=lanes)
+        except gpu.Srt3dError as e:  # a regime the shape does not admit must say so, not compute garbage
+            assert e.code == -3, (c, path, lanes, e)
+            continue
+        torch.cuda.synchronize()
+        _assert_sketch_close(_host(z), zo)
+
+
+@pytest.mark.parametrize("i", range(N_CASES))
+def test_fuzz_grad_and_init(gpu, oracle_mod, inputs_mod, i):
+    """Expected sketch, loss + gradient, fused step == unfused step, and the backprojection on random
+    shapes (m <= 64, K <= 8)."""
+    import torch
+
+    c = _case(i)
+    T, m, K, sigma = c["T"], c["m"], c["K"], c["sigma"]
+    npix = max(c["npix"], 2)
+    t, a = inputs_mod.random_theta(npix, K, T, seed=c["seed"] + 1)
+    z = inputs_mod.random_sketch(npix, m, seed=c["seed"] + 2)
+    dz, dt, da = _dev(z), _dev(t), _dev(a)
+    phi = gpu.srt3d_expected_sketch(dt, da, sigma, T, m)
+    gt, ga, L = gpu.srt3d_sketch_grad(dz, dt, da, sigma, T, m)
+    torch.cuda.synchronize()
+    _assert_sketch_close(_host(phi), oracle_mod.expected_sketch(t, a, sigma, T, m))
+    go = oracle_mod.sketch_grad(z, t, a, sigma, T, m)
+    _grad_tol_check(z, t, a, sigma, T, m, (_host(gt), _host(ga), _host(L)), go)
+    # fused step == gradient + update, bitwise
+    t1, a1 = dt.clone(), da.clone()
+    gpu.srt3d_sketch_grad_step(dz, t1, a1, sigma, T, m, 0.5)
+    t2, a2 = dt.clone(), da.clone()
+    gpu.srt3d_descent_update(t2, a2, gt, ga, sigma, T, m, 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(t1.view(torch.int32), t2.view(torch.int32)) and torch.equal(a1.view(torch.int32),
+                                                                                   a2.view(torch.int32))
+    N = int(np.random.default_rng(c["seed"]).choice([32, 64, 96, 256, 320, 480, 512, 777]))
+    g = gpu.srt3d_backproject(dz, sigma, T, N)
+    torch.cuda.synchronize()
+    gbo = oracle_mod.backproject(z, sigma, T, N)
+    w = 2 * np.pi * np.arange(1, m + 1) / T
+    S = np.sum(np.exp(-(sigma**2) * w**2 / 2) * np.abs(z.astype(np.complex128)), axis=1)[:, None]
+    assert np.all(np.abs(_host(g) - gbo) <= 1e-5 * S + 1e-30), (c, N)

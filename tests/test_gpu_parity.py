@@ -14,6 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 SKETCH_ATOL = 1e-5
+FP32_TINY = float(np.finfo(np.float32).tiny)  # 1.2e-38, smallest normal fp32
 
 
 def _dev(a):
@@ -309,14 +310,16 @@ def _grad_tol_check(z, t, a, sigma, T, m, gg, go):
     S_L = (mag**2).sum(1)
     S_a = 2 * (h[None, :] * mag).sum(1)
     S_t = 2 * np.abs(a64) * ((w * h)[None, :] * mag).sum(1)[:, None]
-    assert np.all(np.abs(L_g - L_o) <= 1e-4 * np.abs(L_o) + 1e-5 * S_L)
-    assert np.all(np.abs(ga_g - ga_o) <= 1e-4 * np.abs(ga_o) + 1e-5 * S_a[:, None])
-    assert np.all(np.abs(gt_g - gt_o) <= 1e-4 * np.abs(gt_o) + 1e-5 * S_t)
+    # + FP32_TINY: components whose exact value lies below fp32's normal range (e.g. hhat_j ~ 1e-78
+    # for sigma = 6 at T = 17) are unrepresentable in the fp32 outputs
+    assert np.all(np.abs(L_g - L_o) <= 1e-4 * np.abs(L_o) + 1e-5 * S_L + FP32_TINY)
+    assert np.all(np.abs(ga_g - ga_o) <= 1e-4 * np.abs(ga_o) + 1e-5 * S_a[:, None] + FP32_TINY)
+    assert np.all(np.abs(gt_g - gt_o) <= 1e-4 * np.abs(gt_o) + 1e-5 * S_t + FP32_TINY)
     # frame level: ||delta||_2 <= 1e-4 ||ref||_2 + 1e-5 ||S||_2 (the floor matters only at the truth,
     # where ref is itself fp32-rounding noise of z)
     for g, o, S in ((gt_g, gt_o, S_t), (ga_g, ga_o, np.broadcast_to(S_a[:, None], ga_o.shape))):
-        assert np.linalg.norm(g - o) <= 1e-4 * np.linalg.norm(o) + 1e-5 * np.linalg.norm(S)
-    assert abs(L_g.sum() - L_o.sum()) <= 1e-4 * L_o.sum() + 1e-5 * S_L.sum()
+        assert np.linalg.norm(g - o) <= 1e-4 * np.linalg.norm(o) + 1e-5 * np.linalg.norm(S) + FP32_TINY * np.sqrt(S.size)
+    assert abs(L_g.sum() - L_o.sum()) <= 1e-4 * L_o.sum() + 1e-5 * S_L.sum() + FP32_TINY * L_o.size
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 8])
