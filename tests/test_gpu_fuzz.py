@@ -88,3 +88,31 @@ def test_fuzz_grad_and_init(gpu, oracle_mod, inputs_mod, i):
     w = 2 * np.pi * np.arange(1, m + 1) / T
     S = np.sum(np.exp(-(sigma**2) * w**2 / 2) * np.abs(z.astype(np.complex128)), axis=1)[:, None]
     assert np.all(np.abs(_host(g) - gbo) <= 1e-5 * S + 1e-30), (c, N)
+
+
+@pytest.mark.parametrize("i", range(N_CASES // 2))
+def test_fuzz_init_depths(gpu, oracle_mod, inputs_mod, i):
+    """Greedy initial depths on random shapes (tensor-core and CUDA-core grids, K <= 8, any min_sep):
+    exact picks unless the oracle faced a near-tie, valid picks always (tests/test_gpu_init.py rules)."""
+    import torch
+
+    from test_gpu_init import _check_picks, _hh
+
+    c = _case(i)
+    T, m, K, sigma = c["T"], c["m"], c["K"], c["sigma"]
+    rng = np.random.default_rng(c["seed"] + 7)
+    N = int(rng.choice([3, 32, 64, 160, 256, 320, 512, 700, 1024]))
+    min_sep = int(rng.choice([0, 1, 10, 50, max(1, T // 8)]))
+    npix = min(max(c["npix"], 2), 1000)
+    bins, offs = inputs_mod.random_csr(npix=npix, T=T, max_n=max(c["max_n"], 50), seed=c["seed"])
+    z = gpu.srt3d_sketch(_dev(bins), _dev(offs), T, m, total_photons=int(offs[-1]))
+    tg, gg, ag, cg = gpu.srt3d_init_depths(z, sigma, T, N, K, min_sep)
+    torch.cuda.synchronize()
+    zh = _host(z)
+    gfull = oracle_mod.backproject(zh, sigma, T, N)
+    to, go, ao, co = oracle_mod.init_depths(gfull, sigma, T, m, K, min_sep)
+    tg, cg = _host(tg), _host(cg)
+    S = np.sum(_hh(sigma, T, m) * np.abs(zh.astype(np.complex128)), axis=1)
+    bad = _check_picks(tg, cg, 2e-5 * S, to.astype(np.float32), co, lambda r: gfull[r], T, N, min_sep)
+    assert bad <= max(2, npix // 20), (c, N, min_sep, bad)
+    assert np.all((_host(ag) >= 0) & (_host(ag) <= 1)) and np.all(cg <= K)
