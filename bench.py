@@ -521,7 +521,10 @@ def run_srt3d(args):
                "pixel_iters_per_s": f.npix * f.iters / (fit_ms * 1e-3),
                "roofline": roofline("srt3d_fit_pixelwise", f_b, f_f, fit_ms),
                "note": "NEXT-2: the iterations of the step in one launch (no spatial regulariser between data "
-                       "steps); bitwise equal to iters x srt3d_sketch_grad_step; timed outside the step"}
+                       "steps); bitwise equal to iters x srt3d_sketch_grad_step; timed outside the step",
+               # the same step (identical theta) with the iterations fused: sketch + one fit launch
+               "step_with_fused_iterations": {"ms": sk_avg + fit_ms, "unit": "photons/s",
+                                              "value": f.n_photons * world / ((sk_avg + fit_ms) * 1e-3)}}
     stream = None
     if stream_ms is not None:
         # bucketing: read each (uint32 pixel, uint16 bin) event once, write its bin, write offsets
