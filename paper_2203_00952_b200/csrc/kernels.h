@@ -65,7 +65,7 @@ struct PixArgs {
   FreqConsts c;
 };
 
-enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3, PX_GRAD_STEP_NL = 4 };  // NL: step without the loss
+enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3, PX_GRAD_STEP_NL = 4, PX_GRAD_NL = 5 };  // NL: no loss output
 
 // Host-side cache of the resident-CTA count of one kernel for the last
 // dynamic shared-memory size asked for (the occupancy query costs several

@@ -218,7 +218,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
     }
     // packed: R = z_j - hh Sk ; L2 += R*R ; RHO = hh R ; SIG = (wh, -wh) * R
     const u64 R = ffma2(pk(-hh, -hh), Sk, pk(zj.x, zj.y));
-    if (MODE != PX_GRAD_STEP_NL) L2 = ffma2(R, R, L2);  // the loss only when it is stored
+    if (MODE != PX_GRAD_STEP_NL && MODE != PX_GRAD_NL) L2 = ffma2(R, R, L2);  // the loss only when it is stored
     const u64 RHO = fmul2(pk(hh, hh), R);   // hhat_j r_j
     const u64 SIG = fmul2(pk(wh, -wh), R);  // omega_j hhat_j (r_r, -r_i)
 #pragma unroll
@@ -240,8 +240,8 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
 template <int K, int MODE>
 __device__ __forceinline__ void pixel_store(const PixArgs& a, long long i, const float (&tk)[K], const float (&ak)[K],
                                             const float (&gt)[K], const float (&ga)[K], float L) {
-  if (MODE != PX_GRAD_STEP_NL && a.loss) a.loss[i] = L;
-  if (MODE == PX_GRAD) {
+  if (MODE != PX_GRAD_STEP_NL && MODE != PX_GRAD_NL && a.loss) a.loss[i] = L;
+  if (MODE == PX_GRAD || MODE == PX_GRAD_NL) {
 #pragma unroll
     for (int k = 0; k < K; k++) {
       a.grad_t[i * K + k] = gt[k];
@@ -621,8 +621,10 @@ cudaError_t launch_pixel(PixMode mode, int K, const PixArgs& a, cudaStream_t s) 
   switch (mode) {
     case PX_EXPECTED:
       return launch_px_k<PX_EXPECTED>(K, a, s);
-    case PX_GRAD:
-      return launch_px_k<PX_GRAD>(K, a, s);
+    case PX_GRAD:  // without a loss output the per-frequency |r|^2 accumulation is compiled out
+      return a.loss ? launch_px_k<PX_GRAD>(K, a, s) : launch_px_k<PX_GRAD_NL>(K, a, s);
+    case PX_GRAD_NL:
+      return launch_px_k<PX_GRAD_NL>(K, a, s);
     case PX_GRAD_STEP:  // without a loss output the per-frequency |r|^2 accumulation is compiled out
       return a.loss ? launch_px_k<PX_GRAD_STEP>(K, a, s) : launch_px_k<PX_GRAD_STEP_NL>(K, a, s);
     case PX_GRAD_STEP_NL:
