@@ -12,7 +12,7 @@ RUNS = [("C1", None), ("C2", None), ("C3", None), ("C5", None)] + [("C4", n) for
 
 def run(cfg, n):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "5", "--warmup", "3",
-           "--no-e2e", "--no-init", "--no-stream", "--cpu-seconds", "6"]
+           "--no-e2e", "--no-init", "--no-stream", "--cpu-seconds", "6"]  # (fit: timed by default)
     if n:
         cmd += ["--n-per-pixel", str(n)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
@@ -41,6 +41,12 @@ def main():
                         f"{g['pixel_iters_per_s']:.3g} px-it/s | {g['gbs']:.0f} | {100 * gr['frac']:.1f} % "
                         f"({gr['bound']}; cold {100 * g['cold_l2_roofline']['frac']:.0f} %) | {clk} MHz | "
                         f"(step, above) | | A12 (tests) |")
+        ft = d.get("fit")
+        if ft:
+            fr = ft["roofline"]
+            rows.append(f"| {name} | fused fit ({ft['iters']} iterations, one launch) | {ft['ms']:.4f} ms | "
+                        f"{ft['pixel_iters_per_s']:.3g} px-it/s | – | {100 * fr['frac']:.1f} % ({fr['bound']}) | "
+                        f"{clk} MHz | | | bitwise = steps (tests) |")
     print("\n".join(rows))
 
 
