@@ -8,7 +8,7 @@
  *           uint32 offsets[npix+1], uint16 bins[nph], float t[npix*K], alpha[npix*K]
  *   output: float z[npix*m*2], grad_t[npix*K], grad_alpha[npix*K], loss[npix]
  *
- * Build: gcc -std=c11 c_api_demo.c -I../include -L../paper_2203_00952_b200 -lsrt3d
+ * Build: gcc -std=c11 c_api_demo.c -I../include -I/usr/local/cuda/include -L../paper_2203_00952_b200 -lsrt3d
  *            -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,<dir of libsrt3d.so>
  */
 #include <cuda_runtime.h>
