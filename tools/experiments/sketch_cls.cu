@@ -1,11 +1,10 @@
-// EXPERIMENT (not built into libsrt3d.so; measured and rejected):
-// K1 class-phased path — photon -> sketch accumulator, Eq. (3),
-// for passes of >= 24 frequencies at ~1e3 photons per pixel (C5), with a
-// caller-provided workspace.  At C5: partition pass 0.74 ms + class-uniform
-// sketch 1.49 ms vs 1.67 ms for the shipped G = 4 kernel — the sketch itself is
-// 11 % faster, but a separate partition pass costs more than that; it pays only
-// where the producer of the CSR frame (e.g. the event bucketing) emits each
-// pixel's photons in class order.
+// EXPERIMENT (not built into libsrt3d.so; with tools/experiments/classed_streaming.patch —
+// `git apply` it and copy this file to paper_2203_00952_b200/csrc/ to rebuild — measured
+// and not shipped, DESIGN.md §5.1 / §5.6).
+// K1 class-phased sketch (srt3d_sketch_classed) — photon -> sketch
+// accumulator, Eq. (3), on a CSR frame whose pixels list
+// their class-A photons first (n_A[i] of them), as srt3d_bucket_events_classed
+// emits it.
 //
 //   z[i][j-1] = (1/n_i) sum_p exp(i 2 pi j x_p / T),  j = j0+1 .. j0+M
 //
@@ -13,111 +12,26 @@
 // one FADD2 per (photon, j) only when every photon of an instruction has the
 // same rotation class (class B: |sin theta| < |cos theta|, chain on
 // theta + pi/2, terms rotated back by (-i)^j); with the class known per
-// photon only at run time, the back-rotation costs two selects per odd term
-// and the body is no faster than the complex power.  Sorting by class inside
-// the sketch kernel costs more than it saves (the class-sorted path).  Here
-// the sort is a separate, HBM-bound pass over the frame:
-//   1. class_partition_kernel: each pixel's photons are written to the
-//      workspace in class order (class A first), n_A[i] recorded — one read
-//      and one write of 2 bytes per photon;
-//   2. sketch_cls_kernel: the grouped kernel (4 lanes per pixel, 16-byte
-//      vector loads, head/tail peel) runs the class-A range with unrotated
-//      chains and then the class-B range with rotated chains — the same
-//      class-uniform body, no selects; since each fp32 partial is zeroed at
-//      a fold, the B range's partials are rotated back (compile-time swizzles
-//      per j) just before their fold.
-// The class of bin x is the integer test on u = 2x mod T (4u < T or 4u > 3T).
+// photon only at run time the back-rotation costs two selects per odd term and
+// the body is no faster than the complex power, and sorting by class costs
+// more than it saves unless the producer of the frame does it for free — the
+// event bucketing keys its per-bucket sort by (pixel, class) at no extra pass.
+// The grouped kernel (4 lanes per pixel, 16-byte vector loads, head/tail
+// peel) runs the class-A range with unrotated chains and then the class-B
+// range with rotated chains — the same class-uniform body, no selects; each
+// fp32 partial is zeroed at a fold, so the B range's partials are rotated back
+// (compile-time swizzles per j) just before their fold.  C5 frame: 1.49 vs
+// 1.67 ms for srt3d_sketch.
 #include <cstdint>
 #include <type_traits>
 #include <utility>
 
-#include "../../paper_2203_00952_b200/csrc/sketch_impl.cuh"
+#include "sketch_impl.cuh"
 
 namespace srt3d {
 
 namespace {
 
-constexpr int CP_WARPS = 8;  // partition pass: warps per CTA, one pixel per warp at a time
-
-__device__ __forceinline__ uint32_t cls_b(uint32_t x, uint32_t T) {
-  const uint32_t u2 = 2u * x;
-  const uint32_t u = min(u2, u2 - T);  // 2x mod T
-  return (4u * u - T) > 2u * T ? 1u : 0u;
-}
-
-// Pass 1: per pixel, photons of class A to the front of the pixel's range in
-// `out` (same offsets as the input), class B to the back; nA[i] = #A.
-__global__ void __launch_bounds__(CP_WARPS * 32) class_partition_kernel(const uint16_t* __restrict__ bins,
-                                                                        const uint32_t* __restrict__ offsets,
-                                                                        long long npix, uint32_t T,
-                                                                        uint16_t* __restrict__ out,
-                                                                        uint32_t* __restrict__ nA) {
-  const int lane = threadIdx.x & 31;
-  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const uint32_t off0 = (uint32_t)(((uintptr_t)bins >> 1) & 7u);
-  const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(bins - off0);
-  uint16_t* const outv = out - offsets[0];  // `out` holds photons offsets[0] .. offsets[npix]
-  for (long long pix = w0; pix < npix; pix += nw) {
-    unsigned long long beg = offsets[pix], end = offsets[pix + 1];
-    if (end < beg) end = beg;
-    const unsigned long long asb = (beg + off0 + 7u) & ~7ull, ase = (end + off0) & ~7ull;
-    unsigned long long hend = end, tbeg = end;
-    long long cb = 0, ce = 0;
-    if (asb < ase) {
-      hend = asb - off0;
-      tbeg = ase - off0;
-      cb = (long long)(asb >> 3);
-      ce = (long long)(ase >> 3);
-    }
-    uint32_t fa = 0, fb = 0;  // warp-uniform fill counts (A from beg up, B from end down)
-    // one round: each lane holds up to 8 photons (vmask), appended in class order
-    auto round = [&](const uint32_t (&wv)[4], uint32_t vmask) {
-      uint32_t isb = 0;
-#pragma unroll
-      for (int i = 0; i < 8; i++) isb |= cls_b((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu, T) << i;
-      isb &= vmask;
-      const uint32_t nb = __popc(isb), na = (uint32_t)__popc(vmask) - nb;
-      uint32_t p = na | (nb << 16), s = p;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, s, d);
-        if (lane >= d) s += t;
-      }
-      const uint32_t tot = __shfl_sync(0xffffffffu, s, 31), ex = s - p;
-      const unsigned long long oa = beg + fa + (ex & 0xffffu);
-      const unsigned long long ob = end - 1 - fb - (ex >> 16);
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        const uint32_t before = __popc(isb & ((1u << i) - 1u));
-        const uint32_t b = (isb >> i) & 1u;
-        const unsigned long long dst = b ? ob - before : oa + (uint64_t)i - before;
-        if ((vmask >> i) & 1u) outv[dst] = (uint16_t)((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-      }
-      fa += tot & 0xffffu;
-      fb += tot >> 16;
-    };
-    {  // head + tail peel: < 16 photons, one per lane
-      const int nh = (int)(hend - beg), nht = nh + (int)(end - tbeg);
-      uint32_t wv[4] = {0, 0, 0, 0};
-      if (lane < nht) wv[0] = bins[lane < nh ? beg + lane : tbeg + (lane - nh)];
-      round(wv, lane < nht ? 1u : 0u);
-    }
-    for (long long c0 = cb; c0 < ce; c0 += 32) {
-      const long long c = c0 + lane;
-      uint32_t wv[4] = {0, 0, 0, 0};
-      if (c < ce) {
-        const uint4 v = __ldcs(vb + c);
-        wv[0] = v.x;
-        wv[1] = v.y;
-        wv[2] = v.z;
-        wv[3] = v.w;
-      }
-      round(wv, c < ce ? 0xffu : 0u);
-    }
-    if (lane == 0) nA[pix] = fa;
-  }
-}
 
 // Class-uniform accumulator: two photons per step, rotated (ROT) or not.
 template <int M>
@@ -183,7 +97,7 @@ __global__ void __launch_bounds__(SK_THREADS, 2) sketch_cls_kernel(SketchArgs a,
   const long long warp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long ntiles = (a.npix + PPW - 1) / PPW;
-  const uint16_t* __restrict__ sb = sbins - a.offsets[0];  // indexed by the frame's offsets
+  const uint16_t* __restrict__ sb = sbins;  // the class-ordered CSR bins, indexed by the frame's offsets
   const uint32_t off0 = (uint32_t)(((uintptr_t)sb >> 1) & 7u);
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(sb - off0);
   const uint32_t T = a.T, j0 = a.j0;
@@ -307,15 +221,6 @@ cudaError_t launch_cls_t(const SketchArgs& a, const uint16_t* sbins, const uint3
 }
 
 }  // namespace
-
-cudaError_t launch_class_partition(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,
-                                   uint16_t* out, uint32_t* nA, cudaStream_t s, int num_sms) {
-  if (npix <= 0) return cudaSuccess;
-  long long grid = (npix + CP_WARPS - 1) / CP_WARPS;
-  if (grid > (long long)num_sms * 8) grid = (long long)num_sms * 8;
-  class_partition_kernel<<<(unsigned)grid, CP_WARPS * 32, 0, s>>>(bins, offsets, npix, T, out, nA);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_sketch_cls(int M, const SketchArgs& a, const uint16_t* sbins, const uint32_t* nA, cudaStream_t s,
                               int num_sms) {
