@@ -6,6 +6,7 @@
 // Each test launches one 1024-thread CTA per SM, reads clock64() around the
 // body and reports lane-ops per clock per SM plus the effective SM clock.
 #include <cstdio>
+#include <string>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -290,10 +291,12 @@ typedef void (*kfn)(float*, float, float, int);
 static void run(const char* name, kfn f, int iters, double lane_ops_per_iter_per_thread, int nsm, float* out, int bs = 1024) {
   dim3 grid(nsm * (1024 / bs)), block(bs);
   f<<<grid, block>>>(out, 1.0000001f, 1e-7f, 8);  // warm
+  CK(cudaGetLastError());  // launch failures (e.g. resources) must not read as a 0-ms run
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
   f<<<grid, block>>>(out, 1.0000001f, 1e-7f, iters);
+  CK(cudaGetLastError());
   cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   static unsigned long long cyc[4096];
@@ -301,11 +304,17 @@ static void run(const char* name, kfn f, int iters, double lane_ops_per_iter_per
   CK(cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(u64) * nb));
   double mx = 0, mean = 0; for (int i = 0; i < nb; i++) { mean += cyc[i]; if (cyc[i] > mx) mx = cyc[i]; }
   mean /= nb;
-  double ops = lane_ops_per_iter_per_thread * iters * 1024.0;  // per SM (all blocks resident)
-  double per_clk = ops / mean;
-  double clk_ghz = mx / (ms * 1e6);
-  double total = ops * nsm / (ms * 1e-3);
-  printf("{\"test\":\"%s\",\"lane_ops_per_clk_per_sm\":%.2f,\"eff_clock_ghz\":%.3f,\"lane_ops_per_s\":%.4e,\"ms\":%.3f}\n", name, per_clk, clk_ghz, total, ms);
+  // rates from the event-timed total (valid whatever the residency); per clock at the 1965 MHz max
+  // clock the pool runs these at (no throttle reasons), and the clock64 view when all blocks of an
+  // SM are co-resident (1024 threads per SM)
+  double total = lane_ops_per_iter_per_thread * iters * (double)bs * (double)nb / (ms * 1e-3);
+  double per_clk = total / (nsm * 1.965e9);
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, bs, 0));
+  const bool resident = per_sm * bs >= 1024;
+  printf("{\"test\":\"%s\",\"lane_ops_per_clk_per_sm\":%.2f,\"lane_ops_per_s\":%.4e,\"ms\":%.3f,"
+         "\"resident_blocks_per_sm\":%d,\"clock64_eff_ghz\":%s}\n", name, per_clk, total, ms, per_sm,
+         resident ? std::to_string(mx / (ms * 1e6)).c_str() : "null");
 }
 
 int main() {
