@@ -13,7 +13,7 @@ from test_gpu_parity import _assert_sketch_close, _dev, _grad_tol_check, _host
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 64
+N_CASES = 128
 
 
 def _case(i):
@@ -113,6 +113,8 @@ def test_fuzz_init_depths(gpu, oracle_mod, inputs_mod, i):
     to, go, ao, co = oracle_mod.init_depths(gfull, sigma, T, m, K, min_sep)
     tg, cg = _host(tg), _host(cg)
     S = np.sum(_hh(sigma, T, m) * np.abs(zh.astype(np.complex128)), axis=1)
-    bad = _check_picks(tg, cg, 2e-5 * S, to.astype(np.float32), co, lambda r: gfull[r], T, N, min_sep)
-    assert bad <= max(2, npix // 20), (c, N, min_sep, bad)
+    # every pixel where the picks differ is checked to be a valid near-tie choice (_check_picks raises
+    # otherwise); no bound on how many: tiny T makes ties structural (T = 2, N = 3: g_1 = g_2 exactly,
+    # and the fp64 oracle breaks the tie by rounding)
+    _check_picks(tg, cg, 2e-5 * S, to.astype(np.float32), co, lambda r: gfull[r], T, N, min_sep)
     assert np.all((_host(ag) >= 0) & (_host(ag) <= 1)) and np.all(cg <= K)
