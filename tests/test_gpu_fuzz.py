@@ -81,6 +81,14 @@ def test_fuzz_grad_and_init(gpu, oracle_mod, inputs_mod, i):
     torch.cuda.synchronize()
     assert torch.equal(t1.view(torch.int32), t2.view(torch.int32)) and torch.equal(a1.view(torch.int32),
                                                                                    a2.view(torch.int32))
+    # fused fit == iterated fused steps, bitwise (NEXT-2)
+    t3, a3 = dt.clone(), da.clone()
+    gpu.srt3d_fit_pixelwise(dz, t3, a3, sigma, T, m, 3, 0.5)
+    for _ in range(2):
+        gpu.srt3d_sketch_grad_step(dz, t1, a1, sigma, T, m, 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(t1.view(torch.int32), t3.view(torch.int32)) and torch.equal(a1.view(torch.int32),
+                                                                                   a3.view(torch.int32))
     N = int(np.random.default_rng(c["seed"]).choice([32, 64, 96, 256, 320, 480, 512, 777]))
     g = gpu.srt3d_backproject(dz, sigma, T, N)
     torch.cuda.synchronize()
