@@ -77,33 +77,16 @@ __device__ __forceinline__ uint32_t phase_q32(float t, double invT) {
   r -= floor(r);                // frac in [0, 1)
   return (uint32_t)(unsigned long long)__double2ll_rn(r * 4294967296.0);  // 2^32 wraps to 0
 }
-// exp(i * 2 pi * q / 2^32): the quadrant is reduced exactly in integers
-// (k = nearest quarter revolution, r = q - k 2^30 in [-2^29, 2^29]), the
-// remainder angle x = r 2 pi / 2^32 (|x| <= pi/4; r rounds to 24 bits, an
-// angle error <= 4.7e-8 rad) goes through Taylor polynomials of degree 9
-// (sin, truncation 1.8e-9) and 10 (cos, 1.2e-10), and the result is rotated
-// by i^k (a swap and signs).  ~20 instructions, and more accurate than
-// sincospif on q 2^-31 (whose fp32 argument keeps only 24 of q's 32 bits).
+// exp(i * 2 pi * q / 2^32) with q interpreted as a signed half-open
+// revolution in [-1/2, 1/2): sincospif on a = q * 2^-31 in [-1, 1).
 // (A 256-entry table + residual polynomial variant, tools/gen_phase_tab.py,
 // was as accurate but slower in the kernel: the dependent global table load
 // sits on the anchor's critical path.)
 __device__ __forceinline__ float2 phasor_q32(uint32_t q) {
-  const uint32_t k = (q + 0x20000000u) >> 30;             // nearest quadrant, 0..3
-  const int32_t r = (int32_t)(q - (k << 30));             // [-2^29, 2^29]
-  const float x = (float)r * 1.4629180792671596e-09f;     // 2 pi / 2^32
-  const float x2 = x * x;
-  float ps = fmaf(x2, 2.75573192e-06f, -1.98412698e-04f);  // 1/9!, -1/7!
-  ps = fmaf(x2, ps, 8.33333333e-03f);                       // 1/5!
-  ps = fmaf(x2, ps, -1.66666667e-01f);                      // -1/3!
-  const float s = fmaf(x * x2, ps, x);
-  float pc = fmaf(x2, -2.75573192e-07f, 2.48015873e-05f);   // -1/10!, 1/8!
-  pc = fmaf(x2, pc, -1.38888889e-03f);                      // -1/6!
-  pc = fmaf(x2, pc, 4.16666667e-02f);                       // 1/4!
-  pc = fmaf(x2, pc, -0.5f);                                 // -1/2!
-  const float c = fmaf(x2, pc, 1.0f);
-  // (c, s) * i^k: k = 1 -> (-s, c), 2 -> (-c, -s), 3 -> (s, -c)
-  const float cr = (k & 1u) ? s : c, sr = (k & 1u) ? c : s;
-  return make_float2(((k + 1u) & 2u) ? -cr : cr, (k & 2u) ? -sr : sr);
+  float a = (float)(int32_t)q * 4.656612873077392578125e-10f;  // 2^-31
+  float s, c;
+  sincospif(a, &s, &c);
+  return make_float2(c, s);
 }
 
 }  // namespace srt3d
