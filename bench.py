@@ -206,7 +206,8 @@ def config_obj(f, args):
                         f" photons/px, SBR={f.sbr}, {f.iters} gradient iterations",
             "npix": f.npix, "photons_per_frame": f.n_photons, "T": f.T, "m": f.m, "K": f.K, "sigma": f.sigma,
             "iters": f.iters, "seed": f.seed, "recipe": f.recipe,
-            "l2": "photon input per step larger than L2 (not flushed); z/theta stay L2-resident across iterations",
+            "l2": "photon input per step larger than L2 (not flushed); in the iteration loop theta stays L2-resident "
+                  "and z streams from HBM every iteration (measured: 67 MB DRAM reads per launch)",
             "parallelism": f"dp{args.gpus} (independent frames per GPU)"}
 
 
@@ -472,8 +473,9 @@ def run_srt3d(args):
         grad = {"kernel": kname, "ms_per_iter": per_iter, "pixel_iters_per_s": f.npix / (per_iter * 1e-3),
                 "gbs": g_bytes / (per_iter * 1e-3) / 1e9, "tflops": g_flops / (per_iter * 1e-3) / 1e12,
                 "roofline": roofline(kname, g_bytes, g_flops, per_iter),
-                "note": "in-loop (CUDA-graph) time per iteration incl. node launch gaps; z/theta stay L2-resident "
-                        "across iterations, so algorithmic bytes / time can exceed the HBM copy peak",
+                "note": "in-loop (CUDA-graph) time per iteration incl. node launch gaps; theta stays L2-resident "
+                        "across iterations, z is re-read from HBM each iteration (71 MB DRAM traffic per launch "
+                        "in the loop vs 80 MB algorithmic)",
                 "cold_l2_ms_per_launch": grad_cold_ms,
                 "cold_l2_roofline": roofline(kname, g_bytes, g_flops, grad_cold_ms) if grad_cold_ms else None}
     init = None
