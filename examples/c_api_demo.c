@@ -78,10 +78,11 @@ int main(int argc, char** argv) {
 
   cudaStream_t s;
   CHECK_CUDA(cudaStreamCreate(&s));
-  CHECK_SRT3D(srt3d_sketch(d_bins, d_offsets, npix, T, m, d_z, nph, s));
+  /* the north-star call: no photon-count hint, the regime is picked on the device */
+  CHECK_SRT3D(srt3d_sketch(d_bins, d_offsets, npix, T, m, d_z, s));
   CHECK_SRT3D(srt3d_sketch_grad(d_z, d_t, d_alpha, npix, K, sigma, T, m, d_gt, d_ga, d_loss, s));
   /* an invalid call fails on the host, side-effect free, with a message */
-  if (srt3d_sketch(d_bins, d_offsets, npix, T, T, d_z, nph, s) != SRT3D_EINVAL) return 4;
+  if (srt3d_sketch(d_bins, d_offsets, npix, T, T, d_z, s) != SRT3D_EINVAL) return 4;
   CHECK_CUDA(cudaStreamSynchronize(s));
 
   float* z = malloc(sizeof(float) * npix * m * 2);

@@ -15,9 +15,13 @@
  *    call returns.
  *  - Calls are asynchronous and stream-ordered: work is enqueued on `stream`
  *    (a cudaStream_t; NULL = the legacy default stream) and the function
- *    returns.  Outputs are valid once the stream has synchronised.  Every
- *    entry point is legal inside CUDA-graph capture, except srt3d_sketch with
- *    total_photons_hint == 0, which reads two offsets back synchronously.
+ *    returns without waiting for the device or reading device memory.
+ *    Outputs are valid once the stream has synchronised.  Every compute entry
+ *    point is legal inside CUDA-graph capture (srt3d_debug_ffma_peak, a
+ *    synchronous measurement utility, is the one exception).
+ *  - Reentrant: no global mutable state except the thread-local error string
+ *    and per-device launch caches (atomics), so any number of host threads
+ *    may call concurrently, on any streams and devices.
  *  - Layouts are row-major.  A sketch / expected sketch is complex64
  *    interleaved (re, im): float z[npix][m][2] (= torch.complex64 (npix, m)).
  *    Parameters are float t[npix][K], float alpha[npix][K].
@@ -76,25 +80,40 @@ const char* srt3d_last_error(void);
  *   T        number of time bins, 2 <= T <= 65536.
  *   m        sketch size, 1 <= m <= min(T - 1, SRT3D_MAX_M).
  *   z        float [npix][m][2] output, 8-byte aligned; fully overwritten.
- *   total_photons_hint  offsets[npix] - offsets[0] if the caller knows it
- *            (selects the launch regime without a device read), else 0.
+ *   stream   cudaStream_t (NULL = legacy default stream).
  * Arithmetic: the phase index r = (j*x) mod T is exact (integer); phasors
  * are fp32, accumulated in fp32 in a fixed (deterministic) order.
- * Errors: SRT3D_EINVAL, SRT3D_ENULL, SRT3D_EUNSUPPORTED, SRT3D_EALIGN,
- *         SRT3D_ECUDA.
+ * Launch regime (DESIGN.md §5.1/§5.3; lanes per pixel or the bin-count path,
+ * chosen from the mean photons per pixel): selected ON THE DEVICE from
+ * offsets[0] and offsets[npix] — the host enqueues the candidate kernels of
+ * each 32-frequency pass and all but one exit at entry.  No host read, no
+ * synchronisation.  srt3d_sketch_ex with a photon-count hint enqueues only
+ * the selected kernel.
+ * Data preconditions (not checked; see the conventions above): a bin >= T
+ * yields unspecified finite values for its pixel, never an out-of-bounds
+ * access.
+ * Errors: SRT3D_EINVAL (T, m, npix), SRT3D_ENULL (bins, offsets or z NULL
+ *         while npix > 0), SRT3D_EUNSUPPORTED (m > SRT3D_MAX_M),
+ *         SRT3D_EALIGN, SRT3D_ECUDA.
  */
 int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m,
-                 float* z, uint64_t total_photons_hint, void* stream);
+                 float* z, void* stream);
 
 /*
- * srt3d_sketch_ex — srt3d_sketch with the launch regime chosen explicitly
- * (same result up to fp32 rounding order; used by tests and tuning):
+ * srt3d_sketch_ex — srt3d_sketch with a host-side photon-count hint and/or
+ * the launch regime chosen explicitly (same result up to fp32 rounding
+ * order; used by the pipeline, tests and tuning):
+ *   total_photons_hint  offsets[npix] - offsets[0] if the caller knows it:
+ *                   the regime is then chosen on the host and only its kernel
+ *                   is enqueued; SRT3D_HINT_UNKNOWN (0) selects on the device
+ *                   as srt3d_sketch does.  A wrong hint changes the launch
+ *                   shape only, never the result.
  *   path            SRT3D_PATH_AUTO (0): bin-count when the mean photon count
  *                   per pixel is >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * T and
  *                   the histogram fits in shared memory, else direct
  *                   (AUTO never selects PAIRED: measured slower);
- *                   SRT3D_PATH_DIRECT (1): per-photon complex recurrence,
- *                   lanes_per_pixel lanes per pixel;
+ *                   SRT3D_PATH_DIRECT (1): per-photon recurrence,
+ *                   lanes_per_pixel lanes per pixel (0: by the photon count);
  *                   SRT3D_PATH_BINCOUNT (2): per-pixel shared-memory
  *                   histogram h[x] then z_j = (1/n) sum_x h[x] e^{i 2 pi j x/T}
  *                   (the same sum as Eq. (3) regrouped by bin; T <= ~17000,
@@ -106,12 +125,14 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  *                   per class (T <= 23800, else
  *                   SRT3D_EUNSUPPORTED).
  *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path only).
+ * Errors as srt3d_sketch, plus SRT3D_EINVAL for an unknown path or lane count.
  */
 #define SRT3D_PATH_AUTO 0
 #define SRT3D_PATH_DIRECT 1
 #define SRT3D_PATH_BINCOUNT 2
 #define SRT3D_PATH_PAIRED 3
 #define SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN 1.0
+#define SRT3D_HINT_UNKNOWN 0ull
 int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
                     uint64_t total_photons_hint, int path, int lanes_per_pixel, void* stream);
 

@@ -33,6 +33,7 @@ _lib = None
 SRT3D_OK = 0
 ERRORS = {-1: "SRT3D_EINVAL", -2: "SRT3D_ENULL", -3: "SRT3D_EUNSUPPORTED", -4: "SRT3D_ECUDA", -5: "SRT3D_EALIGN"}
 PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT, PATH_PAIRED = 0, 1, 2, 3
+HINT_UNKNOWN = 0
 EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
            "srt3d_sketch_grad",
            "srt3d_descent_update", "srt3d_sketch_grad_step", "srt3d_check_csr", "srt3d_debug_phase_index",
@@ -62,7 +63,7 @@ def load_library(path: str | None = None):
     lib.srt3d_version.restype = ctypes.c_int
     lib.srt3d_last_error.argtypes = []
     lib.srt3d_last_error.restype = ctypes.c_char_p
-    lib.srt3d_sketch.argtypes = [P, P, i64, u32, u32, P, u64, P]
+    lib.srt3d_sketch.argtypes = [P, P, i64, u32, u32, P, P]
     lib.srt3d_sketch_ex.argtypes = [P, P, i64, u32, u32, P, u64, ctypes.c_int, ctypes.c_int, P]
     lib.srt3d_expected_sketch.argtypes = [P, P, i64, u32, f32, u32, u32, P, P]
     lib.srt3d_sketch_grad.argtypes = [P, P, P, i64, u32, f32, u32, u32, P, P, P, P]
@@ -111,30 +112,44 @@ def _need_cuda(*ts):
             raise ValueError("all tensors must be contiguous CUDA tensors")
 
 
+def _bins_ptr(bins, offsets):
+    # an empty photon array has no storage; any valid device pointer will do
+    # (no pixel owns a photon, so the kernels never dereference it)
+    return _ptr(bins) if bins.numel() else _ptr(offsets)
+
+
 def srt3d_sketch(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: torch.Tensor | None = None,
                  total_photons: int | None = None, stream=None) -> torch.Tensor:
-    """Eq. (3): complex64 (npix, m) sketch of a uint16/uint32 CSR frame on the GPU."""
+    """Eq. (3): complex64 (npix, m) sketch of a uint16/uint32 CSR frame on the GPU.
+
+    Without ``total_photons`` this is the C ``srt3d_sketch`` (launch regime chosen on
+    the device, no host read); with it, ``srt3d_sketch_ex`` with the hint (only the
+    selected kernel is enqueued)."""
     npix = offsets.numel() - 1
     if z is None:
         z = torch.empty((max(npix, 0), m), dtype=torch.complex64, device=offsets.device)
     _need_cuda(bins, offsets, z)
     assert bins.dtype == torch.uint16 and offsets.dtype == torch.uint32 and z.dtype == torch.complex64
-    hint = int(total_photons) if total_photons is not None else 0
-    _call("srt3d_sketch", _ptr(bins), _ptr(offsets), npix, T, m, _ptr(z), hint, _stream(stream))
+    if total_photons is None:
+        _call("srt3d_sketch", _bins_ptr(bins, offsets), _ptr(offsets), npix, T, m, _ptr(z), _stream(stream))
+    else:
+        _call("srt3d_sketch_ex", _bins_ptr(bins, offsets), _ptr(offsets), npix, T, m, _ptr(z), int(total_photons),
+              PATH_AUTO, 0, _stream(stream))
     return z
 
 
 def srt3d_sketch_ex(bins: torch.Tensor, offsets: torch.Tensor, T: int, m: int, z: torch.Tensor | None = None,
                     total_photons: int | None = None, path: int = PATH_AUTO, lanes_per_pixel: int = 0,
                     stream=None) -> torch.Tensor:
-    """Eq. (3) with the launch regime chosen explicitly (PATH_DIRECT with lanes 4..32, PATH_BINCOUNT, PATH_PAIRED)."""
+    """Eq. (3) with the launch regime chosen explicitly (PATH_DIRECT with lanes 4..32, PATH_BINCOUNT, PATH_PAIRED);
+    total_photons=None: HINT_UNKNOWN (regime picked on the device)."""
     npix = offsets.numel() - 1
     if z is None:
         z = torch.empty((max(npix, 0), m), dtype=torch.complex64, device=offsets.device)
     _need_cuda(bins, offsets, z)
-    hint = int(total_photons) if total_photons is not None else 0
-    _call("srt3d_sketch_ex", _ptr(bins), _ptr(offsets), npix, T, m, _ptr(z), hint, int(path), int(lanes_per_pixel),
-          _stream(stream))
+    hint = int(total_photons) if total_photons is not None else HINT_UNKNOWN
+    _call("srt3d_sketch_ex", _bins_ptr(bins, offsets), _ptr(offsets), npix, T, m, _ptr(z), hint, int(path),
+          int(lanes_per_pixel), _stream(stream))
     return z
 
 

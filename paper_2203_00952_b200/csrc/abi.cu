@@ -27,18 +27,7 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(SRT3D_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
 }
 
-int num_sms_current() {
-  static int cache[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (dev < 0 || dev >= 64) return 148;
-  if (cache[dev] == 0) {
-    int n = 0;
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    cache[dev] = n;
-  }
-  return cache[dev];
-}
+int num_sms_current() { return srt3d::num_sms_device(); }
 
 bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
@@ -86,26 +75,121 @@ void fill_consts(srt3d::PixArgs& a, float sigma, uint32_t T, uint32_t m, float e
   a.max_step = (float)((double)T / (4.0 * (double)m));
 }
 
-int lanes_for(double mean_photons) {
-  // >= ~100 photons per lane amortises the group reduce-scatter and the
-  // head/tail peel (tools/sketch_tune.cu: G=8 beats G=16 at n=1000, m=32)
-  if (mean_photons >= 4096.0) return 32;
-  if (mean_photons >= 2048.0) return 16;
-  if (mean_photons >= 256.0) return 8;
-  return 4;
-}
-
 bool pair_fits(uint32_t T) { return T <= srt3d::SO_MAX_T; }
 
-int choose_path(uint32_t T, uint32_t m, double mean, int* lanes) {
+bool hist_fits(uint32_t T, int M) { return srt3d::sketch_hist_smem(T, M) <= 227u * 1024u; }
+
+// Lanes per pixel of a regime (0: bin-count, one CTA per pixel).
+int regime_lanes(uint32_t rg) {
+  switch (rg) {
+    case srt3d::RG_G4:
+    case srt3d::RG_G4C:
+      return 4;
+    case srt3d::RG_G8:
+      return 8;
+    case srt3d::RG_G16:
+      return 16;
+    case srt3d::RG_G32:
+      return 32;
+    default:
+      return 0;
+  }
+}
+
+cudaError_t launch_regime(uint32_t rg, int M, const srt3d::SketchArgs& a, cudaStream_t s, int nsm) {
+  switch (rg) {
+    case srt3d::RG_G4C:
+      return srt3d::launch_sketch_pass(M, srt3d::SK_G4_CHEB, a, s, nsm);
+    case srt3d::RG_H128:
+      return srt3d::launch_sketch_hist(M, a, 128, s, nsm);
+    case srt3d::RG_H256:
+      return srt3d::launch_sketch_hist(M, a, 256, s, nsm);
+    case srt3d::RG_H512:
+      return srt3d::launch_sketch_hist(M, a, 512, s, nsm);
+    default:
+      return srt3d::launch_sketch_pass(M, regime_lanes(rg), a, s, nsm);
+  }
+}
+
+// Regimes sketch_regime() can return for (npix, T, M, mode) at any photon
+// count: it is piecewise constant in the mean photons per pixel with
+// breakpoints at these means, so evaluating it there finds every candidate.
+int regime_candidates(int64_t npix, uint32_t T, int M, uint32_t mode, uint32_t* out) {
+  const unsigned long long np = (unsigned long long)npix;
+  const unsigned long long means[] = {0, 256, 2048, 4096, T, 30000, 80000};
+  int n = 0;
+  for (unsigned long long mu : means) {
+    const unsigned long long tot = mu * np;
+    if (tot >= (1ull << 32)) continue;  // total photons < 2^32 (precondition)
+    const uint32_t rg = srt3d::sketch_regime(tot, npix, T, M, mode);
+    bool seen = false;
+    for (int i = 0; i < n; i++) seen = seen || out[i] == rg;
+    if (!seen) out[n++] = rg;
+  }
+  return n;
+}
+
+// The sketch entry points.  have_hint: total_photons = offsets[npix] -
+// offsets[0] is known on the host, so the regime is chosen here; otherwise
+// every candidate regime of the pass is launched with rg_want set and each
+// kernel picks itself (or exits) from the two offsets it reads on the device:
+// no host read, no synchronisation, graph-capturable.  A wrong hint changes
+// only the launch shape, never the result (every regime computes Eq. (3)).
+int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
+                 bool have_hint, uint64_t total, int path, int lanes_per_pixel, void* stream) {
+  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
+  int rc = check_tm(T, m);
+  if (rc) return rc;
+  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_PAIRED) return fail(SRT3D_EINVAL, "path=%d unknown", path);
+  if (lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 && lanes_per_pixel != 16 &&
+      lanes_per_pixel != 32)
+    return fail(SRT3D_EINVAL, "lanes_per_pixel=%d must be 0, 4, 8, 16 or 32", lanes_per_pixel);
+  if (npix == 0) return SRT3D_OK;
+  if (!bins || !offsets || !z) return fail(SRT3D_ENULL, "bins/offsets/z must be non-NULL");
+  if (!aligned(bins, 2) || !aligned(offsets, 4) || !aligned(z, 8))
+    return fail(SRT3D_EALIGN, "bins/offsets/z must be 2/4/8-byte aligned");
   const int M0 = (int)(m < 32 ? m : 32);
-  const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
-  int path = SRT3D_PATH_DIRECT;
-  if (hist_fits && mean >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * (double)T) path = SRT3D_PATH_BINCOUNT;
-  int G = lanes_for(mean);
-  if (G == 8 && M0 >= 24) G = 4;  // the G = 4 rotated-Chebyshev regime of srt3d_sketch_ex
-  if (lanes) *lanes = path == SRT3D_PATH_BINCOUNT ? 0 : (path == SRT3D_PATH_PAIRED ? 32 : G);
-  return path;
+  if (path == SRT3D_PATH_BINCOUNT && !hist_fits(T, M0))
+    return fail(SRT3D_EUNSUPPORTED, "bin-count path needs T <= ~17000 (T=%u)", T);
+  if (path == SRT3D_PATH_PAIRED && !pair_fits(T))
+    return fail(SRT3D_EUNSUPPORTED, "class-sorted path needs T <= %u (T=%u)", srt3d::SO_MAX_T, T);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nsm = num_sms_current();
+  srt3d::SketchArgs a = {};
+  a.bins = bins;
+  a.offsets = offsets;
+  a.npix = npix;
+  a.T = T;
+  a.mstride = m;
+  a.z = z;
+  for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+    a.j0 = j0;
+    a.rg_want = srt3d::RG_NONE;
+    const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
+    cudaError_t e = cudaSuccess;
+    if (path == SRT3D_PATH_PAIRED) {
+      e = srt3d::launch_sketch_pair(M, a, s, nsm);
+    } else if (path == SRT3D_PATH_DIRECT && lanes_per_pixel != 0) {
+      e = srt3d::launch_sketch_pass(M, lanes_per_pixel, a, s, nsm);
+    } else {
+      const uint32_t mode = path == SRT3D_PATH_BINCOUNT ? srt3d::RGM_HIST
+                            : (path == SRT3D_PATH_AUTO && hist_fits(T, M)) ? srt3d::RGM_AUTO
+                                                                            : srt3d::RGM_DIRECT;
+      a.rg_mode = mode;
+      if (have_hint) {
+        e = launch_regime(srt3d::sketch_regime(total, npix, T, M, mode), M, a, s, nsm);
+      } else {
+        uint32_t cand[8];
+        const int nc = regime_candidates(npix, T, M, mode, cand);
+        for (int i = 0; i < nc && e == cudaSuccess; i++) {
+          a.rg_want = nc > 1 ? cand[i] : srt3d::RG_NONE;
+          e = launch_regime(cand[i], M, a, s, nsm);
+        }
+      }
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
+  }
+  return SRT3D_OK;
 }
 
 }  // namespace
@@ -116,72 +200,26 @@ int srt3d_version(void) { return 100; }
 
 const char* srt3d_last_error(void) { return g_err; }
 
+int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
+                 void* stream) {
+  return sketch_entry(bins, offsets, npix, T, m, z, false, 0, SRT3D_PATH_AUTO, 0, stream);
+}
+
 int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
                     uint64_t total_photons_hint, int path, int lanes_per_pixel, void* stream) {
-  if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
-  int rc = check_tm(T, m);
-  if (rc) return rc;
-  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_PAIRED) return fail(SRT3D_EINVAL, "path=%d unknown", path);
-  if (lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 && lanes_per_pixel != 16 &&
-      lanes_per_pixel != 32)
-    return fail(SRT3D_EINVAL, "lanes_per_pixel=%d must be 0, 4, 8, 16 or 32", lanes_per_pixel);
-  if (npix == 0) return SRT3D_OK;
-  if (!offsets || !z) return fail(SRT3D_ENULL, "offsets/z must be non-NULL");
-  if (!bins && total_photons_hint != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
-  if (!aligned(bins, 2) || !aligned(offsets, 4) || !aligned(z, 8))
-    return fail(SRT3D_EALIGN, "bins/offsets/z must be 2/4/8-byte aligned");
-  const int M0 = (int)(m < 32 ? m : 32);
-  const bool hist_fits = srt3d::sketch_hist_smem(T, M0) <= 227u * 1024u;
-  if (path == SRT3D_PATH_BINCOUNT && !hist_fits)
-    return fail(SRT3D_EUNSUPPORTED, "bin-count path needs T <= ~17000 (T=%u)", T);
-  if (path == SRT3D_PATH_PAIRED && !pair_fits(T))
-    return fail(SRT3D_EUNSUPPORTED, "class-sorted path needs T <= %u (T=%u)", srt3d::SO_MAX_T, T);
-  cudaStream_t s = (cudaStream_t)stream;
-  uint64_t total = total_photons_hint;
-  if (total == 0 && (path == SRT3D_PATH_AUTO || lanes_per_pixel == 0)) {
-    uint32_t ends[2] = {0, 0};
-    cudaError_t e = cudaMemcpyAsync(&ends[0], offsets, 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&ends[1], offsets + npix, 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch(read offsets)");
-    total = ends[1] >= ends[0] ? (uint64_t)(ends[1] - ends[0]) : 0;
-  }
-  if (!bins && total != 0) return fail(SRT3D_ENULL, "bins must be non-NULL");
-  const double mean = (double)total / (double)npix;
-  if (path == SRT3D_PATH_AUTO) path = choose_path(T, m, mean, nullptr);
-  const int G = lanes_per_pixel ? lanes_per_pixel : lanes_for(mean);
-  const int nsm = num_sms_current();
-  srt3d::SketchArgs a;
-  a.bins = bins ? bins : reinterpret_cast<const uint16_t*>(offsets);  // never dereferenced when no photons
-  a.offsets = offsets;
-  a.npix = npix;
-  a.T = T;
-  a.mstride = m;
-  a.z = z;
-  for (uint32_t j0 = 0; j0 < m; j0 += 32) {
-    a.j0 = j0;
-    const int M = (int)((m - j0) < 32 ? (m - j0) : 32);
-    // auto regime, long passes at ~1e3 photons/pixel: G = 4 + rotated
-    // Chebyshev beats G = 8 + complex power
-    const int Gp = (lanes_per_pixel == 0 && G == 8 && M >= 24) ? srt3d::SK_G4_CHEB : G;
-    cudaError_t e = path == SRT3D_PATH_BINCOUNT ? srt3d::launch_sketch_hist(M, a, mean, s, nsm)
-                    : path == SRT3D_PATH_PAIRED ? srt3d::launch_sketch_pair(M, a, s, nsm)
-                                                : srt3d::launch_sketch_pass(M, Gp, a, s, nsm);
-    if (e != cudaSuccess) return cuda_fail(e, "srt3d_sketch");
-  }
-  return SRT3D_OK;
+  return sketch_entry(bins, offsets, npix, T, m, z, total_photons_hint != SRT3D_HINT_UNKNOWN, total_photons_hint,
+                      path, lanes_per_pixel, stream);
 }
 
 int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photons, int* lanes_per_pixel) {
   if (npix <= 0) return fail(SRT3D_EINVAL, "npix=%lld must be > 0", (long long)npix);
   int rc = check_tm(T, m);
   if (rc) return rc;
-  return choose_path(T, m, (double)total_photons / (double)npix, lanes_per_pixel);
-}
-
-int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
-                 uint64_t total_photons_hint, void* stream) {
-  return srt3d_sketch_ex(bins, offsets, npix, T, m, z, total_photons_hint, SRT3D_PATH_AUTO, 0, stream);
+  const int M0 = (int)(m < 32 ? m : 32);
+  const uint32_t rg = srt3d::sketch_regime(total_photons, npix, T, M0,
+                                           hist_fits(T, M0) ? srt3d::RGM_AUTO : srt3d::RGM_DIRECT);
+  if (lanes_per_pixel) *lanes_per_pixel = regime_lanes(rg);
+  return rg >= srt3d::RG_H128 ? SRT3D_PATH_BINCOUNT : SRT3D_PATH_DIRECT;
 }
 
 int srt3d_expected_sketch(const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,

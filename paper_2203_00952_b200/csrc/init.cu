@@ -249,13 +249,9 @@ __global__ void __launch_bounds__(BP_WARPS * 32) init_k1_kernel(const BpArgs a) 
 cudaError_t launch_init_k1(const BpArgs& a, cudaStream_t s) {
   if (a.npix <= 0) return cudaSuccess;
   const size_t smem = sizeof(float2) * BP_WARPS * 32 * (a.m | 1u);
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(init_k1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(float2) * BP_WARPS * 32 * (MAX_M | 1)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, init_k1_kernel, (int)(sizeof(float2) * BP_WARPS * 32 * (MAX_M | 1)));
+  if (e != cudaSuccess) return e;
   const long long grid = (a.npix + 32 * BP_WARPS - 1) / (32 * BP_WARPS);
   init_k1_kernel<<<(unsigned)grid, BP_WARPS * 32, smem, s>>>(a);
   return cudaGetLastError();
@@ -276,17 +272,14 @@ cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int n
   if (!force_cores && backproject_tc_supported(a.N, a.m)) return launch_backproject_tc(a, pick, s, num_sms);
   const size_t smem = backproject_smem(a.N, pick);
   auto fn = pick ? backproject_kernel<true> : backproject_kernel<false>;
-  static bool attr_set[2] = {false, false};  // benign race: idempotent
-  if (!attr_set[pick]) {
-    // the largest grid the entry points accept: N <= 8192 (backproject), N <= 4096 (picks)
-    const size_t cap = pick ? backproject_smem(4096, true) : backproject_smem(8192, false);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
-    if (e != cudaSuccess) return e;
-    attr_set[pick] = true;
-  }
+  static SmemAttrOnce attr[2];
+  // the largest grid the entry points accept: N <= 8192 (backproject), N <= 4096 (picks)
+  const size_t smem_cap = pick ? backproject_smem(4096, true) : backproject_smem(8192, false);
+  cudaError_t e = smem_attr_once(attr[pick], fn, (int)smem_cap);
+  if (e != cudaSuccess) return e;
   static OccCache occ[2];
   int per_sm = 0;
-  cudaError_t e = occupancy_cached(occ[pick], fn, BP_WARPS * 32, smem, &per_sm);
+  e = occupancy_cached(occ[pick], fn, BP_WARPS * 32, smem, &per_sm);
   if (e != cudaSuccess) return e;
   long long grid = (a.npix + BP_WARPS - 1) / BP_WARPS;
   const long long cap = (long long)per_sm * num_sms;

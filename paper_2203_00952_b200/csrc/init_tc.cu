@@ -468,12 +468,9 @@ bool backproject_tc_supported(uint32_t N, uint32_t m) { return m <= 32 && N % 32
 cudaError_t launch_backproject_tc(const BpArgs& a, bool pick, cudaStream_t s, int num_sms) {
   if (a.npix <= 0) return cudaSuccess;
   auto fn = pick ? bp_tc_kernel<true> : bp_tc_kernel<false>;
-  static bool attr_set[2] = {false, false};  // benign race: idempotent
-  if (!attr_set[pick]) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bp_tc_smem(512, pick));
-    if (e != cudaSuccess) return e;
-    attr_set[pick] = true;
-  }
+  static SmemAttrOnce attr[2];
+  cudaError_t e = smem_attr_once(attr[pick], fn, (int)bp_tc_smem(512, pick));
+  if (e != cudaSuccess) return e;
   const long long tiles = (a.npix + TC_M - 1) / TC_M;
   long long grid = num_sms;  // one persistent CTA per SM (the accumulator holds up to all 512 TMEM columns)
   if (grid > tiles) grid = tiles;

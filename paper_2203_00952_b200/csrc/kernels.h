@@ -1,5 +1,6 @@
 // Internal declarations shared by the kernel translation units and the C ABI.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -33,7 +34,45 @@ struct SketchArgs {
   uint32_t j0;       // first frequency of this pass is j0 + 1
   uint32_t mstride;  // m of the output row
   float* z;
+  // Device-side regime selection (srt3d_sketch without a photon-count hint):
+  // rg_want != RG_NONE makes the kernel exit unless sketch_regime(offsets[npix] -
+  // offsets[0], npix, T, M, rg_mode) == rg_want, so exactly one of the candidate
+  // launches of a pass does the work and the host never reads device memory.
+  uint32_t rg_mode;  // RGM_AUTO / RGM_DIRECT / RGM_HIST
+  uint32_t rg_want;  // RG_NONE: unconditional launch
 };
+
+// ---- launch regimes of the sketch -------------------
+// A function of the frame's photon count, evaluated with exact integer
+// comparisons so the host (with a hint) and the device (from offsets) agree:
+// mean >= X  <=>  total >= X * npix.
+enum : uint32_t { RG_NONE = 0, RG_G4, RG_G8, RG_G16, RG_G32, RG_G4C, RG_H128, RG_H256, RG_H512, RG_COUNT };
+enum : uint32_t { RGM_AUTO = 0, RGM_DIRECT = 1, RGM_HIST = 2 };
+constexpr uint32_t SK_TABLE_MAX_T = 24575;  // (T + 1) float2 entries fit SK_MAX_SMEM
+// mode: RGM_AUTO (bin-count allowed: the host passes it only when the
+// histogram fits in shared memory), RGM_DIRECT, RGM_HIST (bin-count forced).
+__host__ __device__ inline uint32_t sketch_regime(unsigned long long total, long long npix, uint32_t T, int M,
+                                                  uint32_t mode) {
+  const unsigned long long np = npix > 0 ? (unsigned long long)npix : 1ull;
+  const bool hist = mode == RGM_HIST || (mode == RGM_AUTO && total >= (unsigned long long)T * np);
+  if (hist) {
+    if (total < 30000ull * np) return RG_H128;  // CTA size by photons per pixel (tools/hist_tune.cu)
+    if (total < 80000ull * np) return RG_H256;
+    return RG_H512;
+  }
+  if (T > SK_TABLE_MAX_T) return RG_G32;  // no shared phase table: one configuration
+  if (total >= 4096ull * np) return RG_G32;
+  if (total >= 2048ull * np) return RG_G16;
+  if (total >= 256ull * np) return M >= 24 ? RG_G4C : RG_G8;  // G = 4 rotated Chebyshev for long passes
+  return RG_G4;
+}
+
+// Device side: true if this launch is a candidate that was not selected.
+__device__ __forceinline__ bool sketch_regime_skip(const SketchArgs& a, int M) {
+  if (a.rg_want == RG_NONE) return false;
+  const uint32_t tot = a.offsets[a.npix] - a.offsets[0];  // < 2^32 (precondition)
+  return sketch_regime(tot, a.npix, a.T, M, a.rg_mode) != a.rg_want;
+}
 
 // Per-call frequency constants, computed on the host in fp64 and rounded:
 // hh[j-1] = hhat(omega_j) = exp(-sigma^2 omega_j^2 / 2), wh[j-1] = omega_j * hhat(omega_j).
@@ -67,33 +106,69 @@ struct PixArgs {
 
 enum PixMode { PX_EXPECTED = 0, PX_GRAD = 1, PX_GRAD_STEP = 2, PX_UPDATE = 3, PX_GRAD_STEP_NL = 4, PX_GRAD_NL = 5 };  // NL: no loss output
 
-// Host-side cache of the resident-CTA count of one kernel for the last
-// dynamic shared-memory size asked for (the occupancy query costs several
-// microseconds per launch otherwise).  Races are benign: a stale or torn
-// value only changes a persistent grid's size, never a result.
+// Per-device host-side launch caches.  cudaFuncSetAttribute acts on the
+// current device only, and the resident-CTA count is a per-device property, so
+// both are keyed by cudaGetDevice(); entries are lock-free atomics (a race only
+// repeats idempotent work), so concurrent callers on any devices are safe.
+constexpr int MAX_DEVICES = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAX_DEVICES) d = 0;
+  return d;
+}
+
+// "Raise this kernel's dynamic shared-memory limit to `bytes`" once per device.
+struct SmemAttrOnce {
+  std::atomic<int> done[MAX_DEVICES];
+};
+template <typename F>
+inline cudaError_t smem_attr_once(SmemAttrOnce& o, F fn, int bytes) {
+  const int d = current_device();
+  if (o.done[d].load(std::memory_order_acquire)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  o.done[d].store(1, std::memory_order_release);
+  return cudaSuccess;
+}
+
+// Resident CTAs per SM of one kernel for the last dynamic shared-memory size
+// asked for on each device (the occupancy query costs several microseconds per
+// launch otherwise).  One 64-bit word per device: (smem + 1) << 16 | per_sm,
+// so a reader never sees a count paired with another size.
 struct OccCache {
-  size_t smem = ~(size_t)0;
-  int per_sm = 0;
+  std::atomic<unsigned long long> v[MAX_DEVICES];
 };
 template <typename F>
 inline cudaError_t occupancy_cached(OccCache& c, F fn, int threads, size_t smem, int* per_sm) {
-  if (c.smem == smem && c.per_sm > 0) {
-    *per_sm = c.per_sm;
+  const int d = current_device();
+  const unsigned long long cur = c.v[d].load(std::memory_order_relaxed);
+  if (cur != 0 && (cur >> 16) == (unsigned long long)smem + 1) {
+    *per_sm = (int)(cur & 0xffffu);
     return cudaSuccess;
   }
   int v = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem);
   if (e != cudaSuccess) return e;
   if (v < 1) v = 1;
-  c.per_sm = v;
-  c.smem = smem;
+  c.v[d].store((((unsigned long long)smem + 1) << 16) | (unsigned long long)(v & 0xffff), std::memory_order_relaxed);
   *per_sm = v;
   return cudaSuccess;
 }
 
+// SM count of the current device (cached per device).
+inline int num_sms_device() {
+  static std::atomic<int> cache[MAX_DEVICES];
+  const int d = current_device();
+  int n = cache[d].load(std::memory_order_relaxed);
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n <= 0) n = 148;
+  cache[d].store(n, std::memory_order_relaxed);
+  return n;
+}
+
 cudaError_t launch_sketch_pass(int M, int G, const SketchArgs& a, cudaStream_t s, int num_sms);
 cudaError_t measure_ffma_peak(double* tflops, int num_sms);
-cudaError_t launch_sketch_hist(int M, const SketchArgs& a, double mean_photons, cudaStream_t s, int num_sms);
+cudaError_t launch_sketch_hist(int M, const SketchArgs& a, int threads, cudaStream_t s, int num_sms);
 size_t sketch_hist_smem(uint32_t T, int M);
 cudaError_t launch_sketch_pair(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
 size_t sketch_pair_smem(uint32_t T);

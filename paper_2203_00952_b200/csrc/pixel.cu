@@ -364,14 +364,15 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (static cudart).
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  // a function-local static initialised once (thread-safe); the entry point is process-wide
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -425,13 +426,9 @@ static cudaError_t launch_fit_t(const PixArgs& a, int iters, cudaStream_t s) {
   auto fn = fit_kernel<K, M>;
   const int S = zstride(M ? M : (int)a.m);
   const size_t smem = sizeof(float2) * (GRAD_THREADS / 32) * 32 * S;
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(float2) * (GRAD_THREADS / 32) * 32 * zstride(MAX_M)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, fn, (int)(sizeof(float2) * (GRAD_THREADS / 32) * 32 * zstride(MAX_M)));
+  if (e != cudaSuccess) return e;
   const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
   fn<<<(unsigned)grid, GRAD_THREADS, smem, s>>>(a, iters);
   return cudaGetLastError();
@@ -496,16 +493,7 @@ __global__ void __launch_bounds__(PX_THREADS) update_kernel(const PixArgs a) {
   }
 }
 
-static int px_num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int px_num_sms() { return num_sms_device(); }
 
 template <int K, int M, int MODE>
 static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
@@ -518,13 +506,9 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
   const int warps = PX_THREADS / 32;
   if (MODE == PX_EXPECTED) {
     const size_t smem = sizeof(float2) * warps * 32 * S;
-    static bool attr_set = false;  // benign race: idempotent
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(expected_kernel<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(sizeof(float2) * warps * 32 * zstride(MAX_M)));
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
+    static SmemAttrOnce attr;
+    cudaError_t e = smem_attr_once(attr, expected_kernel<K, M>, (int)(sizeof(float2) * warps * 32 * zstride(MAX_M)));
+    if (e != cudaSuccess) return e;
     const long long grid = (a.npix + PX_THREADS - 1) / PX_THREADS;
     expected_kernel<K, M><<<(unsigned)grid, PX_THREADS, smem, s>>>(a);
     return cudaGetLastError();
@@ -545,12 +529,9 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
           auto tfn = grad_kernel_tma<K, M, MODE>;
           const size_t tsmem = 1024 + (size_t)gwarps * (M / 16) * (4096 + 8);
-          static bool tattr = false;
-          if (!tattr) {
-            cudaError_t e = cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-            if (e != cudaSuccess) return e;
-            tattr = true;
-          }
+          static SmemAttrOnce tattr;
+          cudaError_t e = smem_attr_once(tattr, tfn, (int)tsmem);
+          if (e != cudaSuccess) return e;
           const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
           tfn<<<(unsigned)grid, GRAD_THREADS, tsmem, s>>>(a, tm);
           return cudaGetLastError();
@@ -559,12 +540,9 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
     }
   }
   auto fn = grad_kernel<K, M, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, fn, smem_max);
+  if (e != cudaSuccess) return e;
   const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
   fn<<<(unsigned)grid, GRAD_THREADS, smem, s>>>(a);
   return cudaGetLastError();

@@ -65,8 +65,11 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
   constexpr int VL = NVP / 32;
   extern __shared__ float2 tab[];
   const uint32_t T = a.T, j0 = a.j0;
+  // hist[T] is a dump slot for out-of-range bins (precondition violations
+  // count there and are never read back)
   uint32_t* hist = reinterpret_cast<uint32_t*>(tab + T + 1);
-  float* red = reinterpret_cast<float*>(hist + ((T + 3) & ~3u));
+  float* red = reinterpret_cast<float*>(hist + ((T + 4) & ~3u));
+  if (sketch_regime_skip(a, M)) return;  // another candidate launch of this pass does the work
   build_phase_table(tab, T);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float invT = 1.0f / (float)T;
@@ -90,8 +93,8 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
       ce = (long long)(ase >> 3);
     }
     const int nh = (int)(hend - beg), nt = (int)(end - tbeg);
-    if (tid < nh) atomicAdd(&hist[bins[beg + tid]], 1u);
-    else if (tid < nh + nt) atomicAdd(&hist[bins[tbeg + (tid - nh)]], 1u);
+    if (tid < nh) atomicAdd(&hist[min((uint32_t)bins[beg + tid], T)], 1u);
+    else if (tid < nh + nt) atomicAdd(&hist[min((uint32_t)bins[tbeg + (tid - nh)], T)], 1u);
     // 16-byte chunks, HS_UNROLL loads in flight per thread: full rounds, then
     // one predicated round (any photon count keeps its loads in flight)
     long long c = cb + tid;
@@ -104,8 +107,8 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
         const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int h = 0; h < 4; h++) {
-          atomicAdd(&hist[w4[h] & 0xffffu], 1u);
-          atomicAdd(&hist[w4[h] >> 16], 1u);
+          atomicAdd(&hist[min(w4[h] & 0xffffu, T)], 1u);
+          atomicAdd(&hist[min(w4[h] >> 16, T)], 1u);
         }
       }
     }
@@ -120,8 +123,8 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
         const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int h = 0; h < 4; h++) {
-          atomicAdd(&hist[w4[h] & 0xffffu], 1u);
-          atomicAdd(&hist[w4[h] >> 16], 1u);
+          atomicAdd(&hist[min(w4[h] & 0xffffu, T)], 1u);
+          atomicAdd(&hist[min(w4[h] >> 16, T)], 1u);
         }
       }
     }
@@ -169,22 +172,19 @@ __global__ void __launch_bounds__(HS_THREADS) sketch_hist_kernel(SketchArgs a) {
 
 inline size_t sketch_hist_smem_t(uint32_t T, int M, int nthreads) {
   const int NVP = ((2 * M + 31) / 32) * 32;
-  return sizeof(float2) * (T + 1) + sizeof(uint32_t) * ((T + 3) & ~3u) + sizeof(float) * (nthreads / 32) * NVP;
+  return sizeof(float2) * (T + 1) + sizeof(uint32_t) * ((T + 4) & ~3u) + sizeof(float) * (nthreads / 32) * NVP;
 }
 
 template <int M, int HS_THREADS = HS_DEFAULT_THREADS, int HS_UNROLL = HS_DEFAULT_UNROLL>
 static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
   auto fn = sketch_hist_kernel<M, HS_THREADS, HS_UNROLL>;
   const size_t smem = sketch_hist_smem_t(a.T, M, HS_THREADS);
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, fn, 227 * 1024);
+  if (e != cudaSuccess) return e;
   static OccCache occ;
   int per_sm = 0;
-  cudaError_t e = occupancy_cached(occ, fn, HS_THREADS, smem, &per_sm);
+  e = occupancy_cached(occ, fn, HS_THREADS, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   long long grid = (long long)per_sm * num_sms;
@@ -197,22 +197,23 @@ static cudaError_t launch_hist_t(const SketchArgs& a, cudaStream_t s, int num_sm
 #ifndef HS_NO_DISPATCH
 size_t sketch_hist_smem(uint32_t T, int M) { return sketch_hist_smem_t(T, M, 512); }  // largest CTA variant
 
-// CTA size by the mean photons per pixel (tools/hist_tune.cu on B200): large
-// CTAs stream heavy pixels (n ~ 1e5-1e6) best; for n ~ 1e4 the per-pixel DFT,
-// reduction and barriers dominate and more, smaller CTAs per SM win (C3-like
-// frame: 512 threads 1.37 ms, 128 threads 0.86 ms).
+// CTA size by the mean photons per pixel (tools/hist_tune.cu on B200; the
+// thresholds live in sketch_regime): large CTAs stream heavy pixels (n ~
+// 1e5-1e6) best; for n ~ 1e4 the per-pixel DFT, reduction and barriers
+// dominate and more, smaller CTAs per SM win (C3-like frame: 512 threads
+// 1.37 ms, 128 threads 0.86 ms).
 template <int M>
-static cudaError_t launch_hist_m(const SketchArgs& a, double mean, cudaStream_t s, int num_sms) {
-  if (mean < 3.0e4) return launch_hist_t<M, 128, 4>(a, s, num_sms);
-  if (mean < 8.0e4) return launch_hist_t<M, 256, 8>(a, s, num_sms);
+static cudaError_t launch_hist_m(const SketchArgs& a, int threads, cudaStream_t s, int num_sms) {
+  if (threads == 128) return launch_hist_t<M, 128, 4>(a, s, num_sms);
+  if (threads == 256) return launch_hist_t<M, 256, 8>(a, s, num_sms);
   return launch_hist_t<M, 512, 8>(a, s, num_sms);
 }
 
-cudaError_t launch_sketch_hist(int M, const SketchArgs& a, double mean_photons, cudaStream_t s, int num_sms) {
+cudaError_t launch_sketch_hist(int M, const SketchArgs& a, int threads, cudaStream_t s, int num_sms) {
   switch (M) {
 #define SRT3D_CASE(MM) \
   case MM:             \
-    return launch_hist_m<MM>(a, mean_photons, s, num_sms);
+    return launch_hist_m<MM>(a, threads, s, num_sms);
     SRT3D_CASE(1) SRT3D_CASE(2) SRT3D_CASE(3) SRT3D_CASE(4) SRT3D_CASE(5) SRT3D_CASE(6) SRT3D_CASE(7) SRT3D_CASE(8)
     SRT3D_CASE(9) SRT3D_CASE(10) SRT3D_CASE(11) SRT3D_CASE(12) SRT3D_CASE(13) SRT3D_CASE(14) SRT3D_CASE(15)
     SRT3D_CASE(16) SRT3D_CASE(17) SRT3D_CASE(18) SRT3D_CASE(19) SRT3D_CASE(20) SRT3D_CASE(21) SRT3D_CASE(22)

@@ -93,8 +93,10 @@ struct PhotonAcc {
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = 0ull;
   }
+  // r >= T (a bin outside [0, T): precondition violation) reads the zero
+  // entry tab[T] — unspecified but finite values, never an out-of-bounds read
   __device__ __forceinline__ static float2 base(const float2* tab, uint32_t r, uint32_t T) {
-    if (TAB) return tab[r];
+    if (TAB) return tab[min(r, T)];
     if (r >= T) return make_float2(0.f, 0.f);
     return phasor_exact(r, T);
   }
@@ -254,6 +256,7 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int gl) {
 template <int M, int G, bool TAB, int SCH>
 __global__ void __launch_bounds__(SK_THREADS) sketch_kernel(SketchArgs a) {
   extern __shared__ float2 tab[];
+  if (sketch_regime_skip(a, M)) return;  // another candidate launch of this pass does the work
   if (TAB) {
     build_phase_table(tab, a.T);
     __syncthreads();
@@ -368,15 +371,12 @@ template <int M, int G, bool TAB, int SCH>
 static cudaError_t launch_sketch_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
   auto fn = sketch_kernel<M, G, TAB, SCH>;
   const size_t smem = TAB ? sizeof(float2) * (a.T + 1) : 0;
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_MAX_SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, fn, (int)SK_MAX_SMEM);
+  if (e != cudaSuccess) return e;
   static OccCache occ;
   int per_sm = 0;
-  cudaError_t e = occupancy_cached(occ, fn, SK_THREADS, smem, &per_sm);
+  e = occupancy_cached(occ, fn, SK_THREADS, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   constexpr int PPW = 32 / G;

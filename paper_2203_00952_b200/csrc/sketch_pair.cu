@@ -123,7 +123,7 @@ __device__ __forceinline__ void so_append(uint16_t* qb, const uint4 v, uint32_t 
   const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
   uint32_t isb = 0;
 #pragma unroll
-  for (int i = 0; i < 8; i++) isb |= so_class_b((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu, T) << i;
+  for (int i = 0; i < 8; i++) isb |= so_class_b(min((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu, T), T) << i;
   isb &= vmask;
   const uint32_t nb = __popc(isb), na = (uint32_t)__popc(vmask) - nb;
   const uint32_t p = na | (nb << 16);
@@ -139,7 +139,8 @@ __device__ __forceinline__ void so_append(uint16_t* qb, const uint4 v, uint32_t 
   for (int i = 0; i < 8; i++) {  // unconditional store: invalid photons go to the junk slot
     const uint32_t nbefore = __popc(isb & ((1u << i) - 1u));
     const uint32_t dst = (((isb >> i) & 1u) ? ob : oa + (uint32_t)i) - nbefore;
-    qb[((vmask >> i) & 1u) ? dst : (uint32_t)SO_JUNK] = (uint16_t)((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+    // bins >= T (precondition violation) become the absent photon T: zero table entry
+    qb[((vmask >> i) & 1u) ? dst : (uint32_t)SO_JUNK] = (uint16_t)min((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu, T);
   }
   fA += tot & 0xffffu;
   fB += tot >> 16;
@@ -292,16 +293,12 @@ template <int M>
 static cudaError_t launch_sorted_t(const SketchArgs& a, cudaStream_t s, int num_sms) {
   auto fn = sketch_sorted_kernel<M>;
   const size_t smem = sketch_pair_smem(a.T);
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sketch_pair_smem(SO_MAX_T));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, fn, (int)sketch_pair_smem(SO_MAX_T));
+  if (e != cudaSuccess) return e;
   static OccCache occ;
   int per_sm = 0;
-  cudaError_t e = occupancy_cached(occ, fn, SK_THREADS, smem, &per_sm);
+  e = occupancy_cached(occ, fn, SK_THREADS, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   constexpr int PPW = 32 / SO_G;

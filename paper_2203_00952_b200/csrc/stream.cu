@@ -497,15 +497,11 @@ static cudaError_t launch_bucket_two_level(const uint32_t* pix, const uint16_t* 
   if (fg > (long long)num_sms * 16) fg = (long long)num_sms * 16;
   scan_add_kernel<<<(unsigned)fg, 256, 0, s>>>(table, bsum, tn, misc + 1);
   const size_t psmem = sizeof(uint32_t) * BK_TILE + sizeof(uint16_t) * BK_TILE;
-  static bool attr_set = false;  // benign race: idempotent (both attributes use their maximum sizes)
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(bucket_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(uint32_t) * ((size_t)3 * (1u << BK_MAX_S) + BK_TILE)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static SmemAttrOnce attr_p, attr_f;  // both at their maximum sizes
+  e = smem_attr_once(attr_p, partition_kernel, (int)psmem);
+  if (e != cudaSuccess) return e;
+  e = smem_attr_once(attr_f, bucket_fine_kernel, (int)(sizeof(uint32_t) * ((size_t)3 * (1u << BK_MAX_S) + BK_TILE)));
+  if (e != cudaSuccess) return e;
   if (nch > 0) partition_kernel<<<(unsigned)nch, 1024, psmem, s>>>(pix, bins, nev, npix, S, NB, nch, table, temp);
   // with no events the table is all zeros: pass C writes zero offsets
   const size_t smem = sizeof(uint32_t) * ((size_t)3 * (1u << S) + BK_TILE);

@@ -71,12 +71,13 @@ class FramePipeline:
         hint = max(1, round(self.n_photons * (i1 - i0) / max(self.npix, 1)))  # selects the launch regime only
         srt3d_sketch(self.bins, self.offsets[i0:i1 + 1], self.T, self.m, z=self.z[i0:i1], total_photons=hint)
 
-    def _iterate(self, i0: int = 0, i1: int | None = None):
+    def _iterate(self, i0: int = 0, i1: int | None = None, iters: int | None = None, reset: bool = True):
         i1 = self.npix if i1 is None else i1
         z, t, a, gt, ga = self.z[i0:i1], self.t[i0:i1], self.a[i0:i1], self.gt[i0:i1], self.ga[i0:i1]
-        t.copy_(self.t0[i0:i1])
-        a.copy_(self.a0[i0:i1])
-        for _ in range(self.iters):
+        if reset:
+            t.copy_(self.t0[i0:i1])
+            a.copy_(self.a0[i0:i1])
+        for _ in range(self.iters if iters is None else int(iters)):
             if self.fused:
                 srt3d_sketch_grad_step(z, t, a, self.sigma, self.T, self.m, self.eta)
             else:
@@ -117,6 +118,12 @@ class FramePipeline:
     def run_device(self):
         self.sketch_phase()
         self.iterate_phase()
+
+    def run_iterations(self, n: int, reset: bool = False):
+        """Enqueue n more iterations of the step's own kernel on self.stream without
+        graphs (reset=True first restores theta0): for per-iteration snapshots in tests."""
+        with torch.cuda.stream(self.stream):
+            self._iterate(iters=n, reset=reset)
 
     def capture_chunks(self, chunks: int):
         """Per-block graphs (sketch + theta reset + iterations) for run_host(chunks=...)."""

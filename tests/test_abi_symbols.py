@@ -81,13 +81,16 @@ def test_host_validation_without_gpu():
 
     lib = p.load_library()
     dummy = ctypes.c_void_p(16)
-    assert lib.srt3d_sketch(dummy, dummy, 4, 1, 1, dummy, 0, None) == -1        # T < 2
-    assert lib.srt3d_sketch(dummy, dummy, 4, 100, 100, dummy, 0, None) == -1    # m >= T
-    assert lib.srt3d_sketch(dummy, dummy, 4, 1000, 65, dummy, 0, None) == -3    # m > MAX_M
-    assert lib.srt3d_sketch(dummy, dummy, -1, 100, 3, dummy, 0, None) == -1     # npix < 0
-    assert lib.srt3d_sketch(None, None, 0, 100, 3, None, 0, None) == 0          # npix = 0 no-op
-    assert lib.srt3d_sketch(dummy, None, 4, 100, 3, dummy, 0, None) == -2       # NULL offsets
-    assert lib.srt3d_sketch(dummy, ctypes.c_void_p(18), 4, 100, 3, dummy, 0, None) == -5  # misaligned offsets
+    assert lib.srt3d_sketch(dummy, dummy, 4, 1, 1, dummy, None) == -1        # T < 2
+    assert lib.srt3d_sketch(dummy, dummy, 4, 100, 100, dummy, None) == -1    # m >= T
+    assert lib.srt3d_sketch(dummy, dummy, 4, 1000, 65, dummy, None) == -3    # m > MAX_M
+    assert lib.srt3d_sketch(dummy, dummy, -1, 100, 3, dummy, None) == -1     # npix < 0
+    assert lib.srt3d_sketch(None, None, 0, 100, 3, None, None) == 0          # npix = 0 no-op
+    assert lib.srt3d_sketch(dummy, None, 4, 100, 3, dummy, None) == -2       # NULL offsets
+    assert lib.srt3d_sketch(None, dummy, 4, 100, 3, dummy, None) == -2       # NULL bins (photon count unknown)
+    assert lib.srt3d_sketch_ex(None, dummy, 4, 100, 3, dummy, 0, 0, 0, None) == -2
+    assert lib.srt3d_sketch_ex(None, dummy, 4, 100, 3, dummy, 5, 1, 4, None) == -2
+    assert lib.srt3d_sketch(dummy, ctypes.c_void_p(18), 4, 100, 3, dummy, None) == -5  # misaligned offsets
     assert lib.srt3d_sketch_grad(dummy, dummy, dummy, 4, 9, ctypes.c_float(1.0), 100, 3, dummy, dummy, None, None) == -3
     assert lib.srt3d_sketch_grad(dummy, dummy, dummy, 4, 2, ctypes.c_float(float("inf")), 100, 3, dummy, dummy,
                                  None, None) == -1

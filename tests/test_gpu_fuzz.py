@@ -121,8 +121,12 @@ def test_fuzz_init_depths(gpu, oracle_mod, inputs_mod, i):
     to, go, ao, co = oracle_mod.init_depths(gfull, sigma, T, m, K, min_sep)
     tg, cg = _host(tg), _host(cg)
     S = np.sum(_hh(sigma, T, m) * np.abs(zh.astype(np.complex128)), axis=1)
-    # every pixel where the picks differ is checked to be a valid near-tie choice (_check_picks raises
-    # otherwise); no bound on how many: tiny T makes ties structural (T = 2, N = 3: g_1 = g_2 exactly,
-    # and the fp64 oracle breaks the tie by rounding)
-    _check_picks(tg, cg, 2e-5 * S, to.astype(np.float32), co, lambda r: gfull[r], T, N, min_sep)
+    # every pixel where the picks differ is checked to be a valid greedy choice within tolerance
+    # (_check_picks raises otherwise); their number is bounded except on shapes where ties are
+    # structural: T < 8 (T = 2, N = 3: g_1 = g_2 exactly, the fp64 oracle breaks the tie by
+    # rounding) or N <= 2m (a grid no finer than the sketch's band: neighbouring grid values of
+    # g coincide to rounding)
+    bad = _check_picks(tg, cg, 2e-5 * S, to.astype(np.float32), co, lambda r: gfull[r], T, N, min_sep)
+    if T >= 8 and N > 2 * m:
+        assert bad <= max(2, npix // 20), (c, N, min_sep, bad)
     assert np.all((_host(ag) >= 0) & (_host(ag) <= 1)) and np.all(cg <= K)

@@ -84,25 +84,48 @@ def test_backproject_tc_many_tiles(gpu, oracle_mod, inputs_mod):
 
 
 def _check_picks(tg, cg, tol_g, to, co, go_row_fn, T, N, min_sep):
-    """Exact match unless the oracle faced a near-tie; then the GPU's pick must be valid."""
+    """Exact match with the oracle's picks, or else the GPU's picks must be a greedy pick
+    sequence (reading A19) of the oracle's g within tolerance tol (the GPU's g differs from
+    the oracle's by <= tol): taken in descending g, each pick
+      * is a candidate within tol (g > -tol, g > g_prev - tol, g >= g_next - tol),
+      * keeps the minimum separation to every earlier pick,
+      * is no smaller (beyond 2 tol) than any certain candidate (g > tol, g > g_prev + tol,
+        g >= g_next + tol) still available after the earlier picks,
+    and if fewer than K picks were made, no certain candidate remains available.  Counts
+    that differ from the oracle's are accepted only under these rules.  Returns the number
+    of pixels that did not match exactly (callers bound it)."""
+    K = tg.shape[1]
     bad = 0
     for i in range(tg.shape[0]):
         if cg[i] == co[i] and np.array_equal(tg[i], to[i]):
             continue
         g = go_row_fn(i)
+        tol = float(tol_g[i])
         n_g = np.rint(tg[i, : cg[i]] * N / T).astype(np.int64) % N
-        cand = (g > -tol_g[i]) & (g >= np.roll(g, 1) - tol_g[i]) & (g >= np.roll(g, -1) - tol_g[i])
-        assert np.all(cand[n_g]), i
-        for a in range(len(n_g)):
-            for b in range(a + 1, len(n_g)):
-                d = abs(n_g[a] - n_g[b])
-                assert min(d, N - d) * T >= min_sep * N, i
-        # a near-tie: the best oracle value among GPU picks and oracle picks agree within tol
-        gg = np.sort(g[n_g])[::-1]
-        n_o = np.rint(to[i, : co[i]] * N / T).astype(np.int64) % N
-        oo = np.sort(g[n_o])[::-1]
-        k = min(len(gg), len(oo))
-        assert np.all(np.abs(gg[:k] - oo[:k]) <= 4 * tol_g[i]) or abs(int(cg[i]) - int(co[i])) <= 1, i
+        gp, gn = np.roll(g, 1), np.roll(g, -1)
+        loose = (g > -tol) & (g > gp - tol) & (g >= gn - tol)
+        certain = (g > tol) & (g > gp + tol) & (g >= gn + tol)
+        grid = np.arange(N)
+
+        def available(taken):
+            ok = certain.copy()
+            for q in taken:
+                d = np.abs(grid - q)
+                ok &= np.minimum(d, N - d) * T >= min_sep * N
+            return ok
+
+        taken = []
+        for n in n_g[np.argsort(-g[n_g], kind="stable")]:
+            assert loose[n], (i, int(n), "not a candidate")
+            for q in taken:
+                d = abs(int(n) - q)
+                assert min(d, N - d) * T >= min_sep * N, (i, int(n), "separation")
+            av = available(taken)
+            if av.any():
+                assert g[n] >= g[av].max() - 2 * tol, (i, int(n), "a clearly larger candidate was available")
+            taken.append(int(n))
+        if len(taken) < K:
+            assert not available(taken).any(), (i, "stopped early although a certain candidate remained")
         bad += 1
     return bad
 

@@ -1,12 +1,16 @@
 """GPU <-> oracle parity through the C ABI (libsrt3d.so), element by element on
 the same seeded inputs.
 
-Tolerances:
+Tolerances (reading A12 = SURVEY.md §8(c) A12):
   * integer phase index: bit-exact (==)
   * sketch / expected sketch: |delta| <= 1e-5 absolute per component (BASELINE north_star)
-  * loss / gradients: |delta| <= 1e-4 |ref| + 1e-5 * S per component, where S is the sum of
-    absolute terms of that component (reading A12; the floor is 5x the worst-case fp32
-    phasor error bound 2e-6 * S), plus frame-level ||delta||_2 / ||ref||_2 <= 1e-4.
+  * loss / gradients, per component: |delta| <= 1e-4 |ref| + 1e-6 * S, where S is the sum
+    of absolute terms of that component (A12);
+  * frame level: ||delta||_2 <= 1e-4 ||ref||_2 wherever fp32 can meet it, i.e. where the
+    evaluation's condition number kappa = ||S||_2 / ||ref||_2 <= 100 (the per-component
+    floor 1e-6 S is then <= 1e-4 of the gradient); at and near the optimum (kappa > 100:
+    r = z - Phi cancels, so fp32 inputs alone carry ~1e-7 S of error) the frame-level
+    check is ||delta||_2 <= 1e-4 ||ref||_2 + 1e-6 ||S||_2.
 """
 import numpy as np
 import pytest
@@ -258,10 +262,13 @@ def test_sketch_empty_frame_and_errors(gpu):
     lib = gpu.load_library()
     import ctypes
 
-    rc = lib.srt3d_sketch(None, ctypes.c_void_p(offs.data_ptr()), 4, 100, 3, ctypes.c_void_p(z.data_ptr()), 3, None)
+    rc = lib.srt3d_sketch(None, ctypes.c_void_p(offs.data_ptr()), 4, 100, 3, ctypes.c_void_p(z.data_ptr()), None)
+    assert rc == -2
+    rc = lib.srt3d_sketch_ex(None, ctypes.c_void_p(offs.data_ptr()), 4, 100, 3, ctypes.c_void_p(z.data_ptr()), 3, 0,
+                             0, None)
     assert rc == -2
     rc = lib.srt3d_sketch(ctypes.c_void_p(bins.data_ptr()), ctypes.c_void_p(offs.data_ptr() + 1), 4, 100, 3,
-                          ctypes.c_void_p(z.data_ptr()), 3, None)
+                          ctypes.c_void_p(z.data_ptr()), None)
     assert rc == -5
     torch.cuda.synchronize()
     assert torch.all(z == 7.0 + 7.0j)
@@ -299,10 +306,11 @@ def test_expected_sketch_parity(gpu, oracle_mod, inputs_mod, K, T, m, sigma):
 
 
 # ----------------------------------------------------------- gradient K3
-def _grad_tol_check(z, t, a, sigma, T, m, gg, go):
-    """A12 per-component tolerance with the S-scaled floor, plus frame-level relative norms."""
-    gt_g, ga_g, L_g = gg
-    gt_o, ga_o, L_o = go
+GRAD_REL, GRAD_FLOOR, KAPPA_PURE = 1e-4, 1e-6, 100.0
+
+
+def _grad_S(z, a, sigma, T, m):
+    """A12 scales: S_L (npix,), S_a (npix,), S_t (npix, K) — sums of absolute terms."""
     w = 2 * np.pi * np.arange(1, m + 1) / T
     h = np.exp(-sigma**2 * w**2 / 2)
     a64 = a.astype(np.float64)
@@ -310,16 +318,35 @@ def _grad_tol_check(z, t, a, sigma, T, m, gg, go):
     S_L = (mag**2).sum(1)
     S_a = 2 * (h[None, :] * mag).sum(1)
     S_t = 2 * np.abs(a64) * ((w * h)[None, :] * mag).sum(1)[:, None]
+    return S_L, S_a, S_t
+
+
+def _grad_tol_check(z, t, a, sigma, T, m, gg, go, what=""):
+    """A12: per component |d| <= 1e-4 |ref| + 1e-6 S; frame level as in the module doc.
+    Returns the worst per-component |d| / S (diagnostic, printed by -s runs)."""
+    gt_g, ga_g, L_g = gg
+    gt_o, ga_o, L_o = go
+    S_L, S_a, S_t = _grad_S(z, a, sigma, T, m)
+    S_a2 = np.broadcast_to(S_a[:, None], ga_o.shape)
+    worst = 0.0
     # + FP32_TINY: components whose exact value lies below fp32's normal range (e.g. hhat_j ~ 1e-78
     # for sigma = 6 at T = 17) are unrepresentable in the fp32 outputs
-    assert np.all(np.abs(L_g - L_o) <= 1e-4 * np.abs(L_o) + 1e-5 * S_L + FP32_TINY)
-    assert np.all(np.abs(ga_g - ga_o) <= 1e-4 * np.abs(ga_o) + 1e-5 * S_a[:, None] + FP32_TINY)
-    assert np.all(np.abs(gt_g - gt_o) <= 1e-4 * np.abs(gt_o) + 1e-5 * S_t + FP32_TINY)
-    # frame level: ||delta||_2 <= 1e-4 ||ref||_2 + 1e-5 ||S||_2 (the floor matters only at the truth,
-    # where ref is itself fp32-rounding noise of z)
-    for g, o, S in ((gt_g, gt_o, S_t), (ga_g, ga_o, np.broadcast_to(S_a[:, None], ga_o.shape))):
-        assert np.linalg.norm(g - o) <= 1e-4 * np.linalg.norm(o) + 1e-5 * np.linalg.norm(S) + FP32_TINY * np.sqrt(S.size)
-    assert abs(L_g.sum() - L_o.sum()) <= 1e-4 * L_o.sum() + 1e-5 * S_L.sum() + FP32_TINY * L_o.size
+    for name, g, o, S in (("loss", L_g, L_o, S_L), ("grad_alpha", ga_g, ga_o, S_a2), ("grad_t", gt_g, gt_o, S_t)):
+        d = np.abs(g.astype(np.float64) - o)
+        lim = GRAD_REL * np.abs(o) + GRAD_FLOOR * S + FP32_TINY
+        bad = d > lim
+        assert not bad.any(), (f"{what} {name}: {int(bad.sum())} components fail A12; worst |d|/lim = "
+                               f"{float((d / lim).max()):.3g}")
+        worst = max(worst, float((d / np.maximum(S, FP32_TINY)).max(initial=0)))
+    for name, g, o, S in (("grad_t", gt_g, gt_o, S_t), ("grad_alpha", ga_g, ga_o, S_a2)):
+        dn, on, Sn = np.linalg.norm(g - o), np.linalg.norm(o), np.linalg.norm(S)
+        kappa = Sn / max(on, 1e-300)
+        lim = GRAD_REL * on + (0.0 if kappa <= KAPPA_PURE else GRAD_FLOOR * Sn) + FP32_TINY * np.sqrt(S.size)
+        assert dn <= lim, f"{what} {name}: frame ||d||/||ref|| = {dn / max(on, 1e-300):.3g} (kappa {kappa:.3g})"
+    dl, lo = abs(L_g.astype(np.float64).sum() - L_o.sum()), L_o.sum()
+    kl = S_L.sum() / max(lo, 1e-300)
+    assert dl <= GRAD_REL * lo + (0.0 if kl <= KAPPA_PURE else GRAD_FLOOR * S_L.sum()) + FP32_TINY * L_o.size, what
+    return worst
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 8])
@@ -526,6 +553,76 @@ def test_config_parity_full_size(gpu, oracle_mod, inputs_mod, name, n):
         go = oracle_mod.sketch_grad(zg[idx], t0[idx], a0[idx], f.sigma, f.T, f.m)
         _grad_tol_check(zg[idx], t0[idx], a0[idx], f.sigma, f.T, f.m,
                         (_host(gt)[idx], _host(ga)[idx], _host(L)[idx]), go)
+
+
+def _update_tol(t, a, go, S_t, S_a, sigma, T, m, eta):
+    """Bound on |theta_{i+1} - oracle_update(theta_i, oracle_grad(theta_i))| implied by the A12
+    gradient tolerance pushed through the (1-Lipschitz-clamped) A13 update, plus fp32 rounding."""
+    w = 2 * np.pi * np.arange(1, m + 1) / T
+    h = np.exp(-sigma**2 * w**2 / 2)
+    gt_o, ga_o, _ = go
+    tol_gt = GRAD_REL * np.abs(gt_o) + GRAD_FLOOR * S_t
+    tol_ga = GRAD_REL * np.abs(ga_o) + GRAD_FLOOR * S_a[:, None]
+    at = eta * tol_gt / (2 * np.maximum(a.astype(np.float64), 0.05) ** 2 * np.sum(w**2 * h**2))
+    aa = eta * tol_ga / (2 * np.sum(h**2))
+    ulp_t = np.spacing(np.float32(T)).astype(np.float64)
+    return at + 2 * ulp_t, aa + 2 * np.spacing(np.float32(1.0)).astype(np.float64)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
+def test_config_per_iteration_parity(gpu, oracle_mod, inputs_mod, name):
+    """SURVEY §4 T2 at full size, on the bench's own FramePipeline step (the fused no-loss
+    gradient + update kernel the bench times; TMA z staging at m = 32): theta_i snapshots at
+    i in {0, 1, iters/2, iters-1} of the real loop.  On sampled pixels:
+      (a) srt3d_sketch_grad(z, theta_i) vs oracle.sketch_grad (A12, module doc);
+      (b) the timed kernel's own step theta_i -> theta_{i+1} vs the oracle's update of theta_i
+          with the oracle's gradient, within the A12 tolerance propagated through the update."""
+    import torch
+
+    from paper_2203_00952_b200.pipeline import FramePipeline
+
+    f = inputs_mod.make_frame(name)
+    t0, a0 = f.theta0()
+    pipe = FramePipeline(f.n_photons, f.npix, f.K, f.T, f.m, f.sigma, iters=f.iters)
+    pipe.load_device(_dev(f.bins), _dev(f.offsets), _dev(t0), _dev(a0))
+    pipe.capture()
+    pipe.run_device()  # the bench step: sketch graph + iteration graph
+    pipe.stream.synchronize()
+    t_fin_graph = _host(pipe.t).copy()
+    zg = _host(pipe.z)
+    idx = _sample_idx(f.npix, 256, seed=2)
+    snaps = sorted({0, 1, f.iters // 2, f.iters - 1})
+    pipe.run_iterations(0, reset=True)
+    done, worst = 0, 0.0
+    zs = zg[idx]
+    S_L, S_a, S_t = None, None, None
+    for i in snaps:
+        pipe.run_iterations(i - done)
+        pipe.stream.synchronize()
+        ti, ai = _host(pipe.t).copy(), _host(pipe.a).copy()
+        gt, ga, L = gpu.srt3d_sketch_grad(pipe.z, pipe.t, pipe.a, f.sigma, f.T, f.m)
+        torch.cuda.synchronize()
+        go = oracle_mod.sketch_grad(zs, ti[idx], ai[idx], f.sigma, f.T, f.m)
+        worst = max(worst, _grad_tol_check(zs, ti[idx], ai[idx], f.sigma, f.T, f.m,
+                                           (_host(gt)[idx], _host(ga)[idx], _host(L)[idx]), go, what=f"{name} i={i}"))
+        # (b) one step of the timed kernel from theta_i
+        pipe.run_iterations(1)
+        pipe.stream.synchronize()
+        done = i + 1
+        t1, a1 = _host(pipe.t)[idx], _host(pipe.a)[idx]
+        to, ao = oracle_mod.descent_update(ti[idx], ai[idx], go[0], go[1], f.sigma, f.T, f.m, eta=0.5)
+        _, S_a, S_t = _grad_S(zs, ai[idx], f.sigma, f.T, f.m)
+        tol_t, tol_a = _update_tol(ti[idx], ai[idx], go, S_t, S_a, f.sigma, f.T, f.m, 0.5)
+        dt = np.abs(t1.astype(np.float64) - to)
+        dt = np.minimum(dt, f.T - dt)
+        assert np.all(dt <= tol_t), (name, i, float((dt / tol_t).max()))
+        assert np.all(np.abs(a1.astype(np.float64) - ao) <= tol_a), (name, i)
+    # the eager snapshots run the same kernel as the captured loop: continuing to iters
+    # reproduces the graph's final theta bitwise
+    pipe.run_iterations(f.iters - done)
+    pipe.stream.synchronize()
+    assert np.array_equal(_host(pipe.t).view(np.uint32), t_fin_graph.view(np.uint32))
+    print(f"{name}: worst per-component |d|/S over iterations {snaps}: {worst:.3g}")
 
 
 def test_pipeline_chained_frames(gpu, inputs_mod):
