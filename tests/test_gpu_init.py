@@ -100,7 +100,9 @@ def _check_picks(tg, cg, tol_g, to, co, go_row_fn, T, N, min_sep):
         if cg[i] == co[i] and np.array_equal(tg[i], to[i]):
             continue
         g = go_row_fn(i)
-        tol = float(tol_g[i])
+        # + the smallest normal fp32: g values below fp32's normal range (hhat ~ 1e-77 at T = 2,
+        # sigma = 6) flush to zero on the GPU and cannot decide a pick
+        tol = float(tol_g[i]) + float(np.finfo(np.float32).tiny)
         n_g = np.rint(tg[i, : cg[i]] * N / T).astype(np.int64) % N
         gp, gn = np.roll(g, 1), np.roll(g, -1)
         loose = (g > -tol) & (g > gp - tol) & (g >= gn - tol)
