@@ -110,8 +110,10 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  *                   shape only, never the result.
  *   path            SRT3D_PATH_AUTO (0): bin-count when the mean photon count
  *                   per pixel is >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * T and
- *                   the histogram fits in shared memory, else direct
- *                   (AUTO never selects PAIRED: measured slower);
+ *                   the histogram fits in shared memory; else ROUTED for a
+ *                   first pass of >= 24 frequencies at 256..2047 photons per
+ *                   pixel where it applies; else direct (AUTO never selects
+ *                   PAIRED: measured slower);
  *                   SRT3D_PATH_DIRECT (1): per-photon recurrence,
  *                   lanes_per_pixel lanes per pixel (0: by the photon count);
  *                   SRT3D_PATH_BINCOUNT (2): per-pixel shared-memory
@@ -124,13 +126,22 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  *                   rotated Chebyshev loops with one accumulator frame switch
  *                   per class (T <= 23800, else
  *                   SRT3D_EUNSUPPORTED).
- *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path only).
+ *                   SRT3D_PATH_ROUTED (4): the direct sum, a lane pair per
+ *                   pixel, each lane's accumulators in one of two rotation
+ *                   frames and every photon routed (shared memory) to a lane
+ *                   whose frame keeps its Chebyshev recurrence accurate:
+ *                   one FFMA2 + one FADD2 per (photon, j) (
+ *                   T % 4 == 0 and T <= 12000, else SRT3D_EUNSUPPORTED;
+ *                   passes after the first 32 frequencies run the direct
+ *                   path).
+ *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path); 0 or 2 (routed).
  * Errors as srt3d_sketch, plus SRT3D_EINVAL for an unknown path or lane count.
  */
 #define SRT3D_PATH_AUTO 0
 #define SRT3D_PATH_DIRECT 1
 #define SRT3D_PATH_BINCOUNT 2
 #define SRT3D_PATH_PAIRED 3
+#define SRT3D_PATH_ROUTED 4
 #define SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN 1.0
 #define SRT3D_HINT_UNKNOWN 0ull
 int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,
@@ -138,11 +149,11 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
 
 /*
  * srt3d_sketch_plan — host-only query: the path (SRT3D_PATH_DIRECT,
- * SRT3D_PATH_BINCOUNT or SRT3D_PATH_PAIRED) and lanes per pixel srt3d_sketch would use for a frame
- * of npix pixels and total_photons photons.  Returns the path (> 0) or a
- * negative error code; *lanes_per_pixel (may be NULL) receives the lane count
- * (0 for the bin-count path, which uses one CTA per pixel; 32 for the
- * paired path, one warp per pixel).
+ * SRT3D_PATH_BINCOUNT or SRT3D_PATH_ROUTED) and lanes per pixel srt3d_sketch
+ * would use for the first 32-frequency pass of a frame of npix pixels and
+ * total_photons photons.  Returns the path (> 0) or a negative error code;
+ * *lanes_per_pixel (may be NULL) receives the lane count (0 for the
+ * bin-count path, which uses one CTA per pixel; 2 for the routed path).
  */
 int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photons, int* lanes_per_pixel);
 

@@ -85,6 +85,8 @@ int regime_lanes(uint32_t rg) {
     case srt3d::RG_G4:
     case srt3d::RG_G4C:
       return 4;
+    case srt3d::RG_RT:
+      return 2;
     case srt3d::RG_G8:
       return 8;
     case srt3d::RG_G16:
@@ -100,6 +102,8 @@ cudaError_t launch_regime(uint32_t rg, int M, const srt3d::SketchArgs& a, cudaSt
   switch (rg) {
     case srt3d::RG_G4C:
       return srt3d::launch_sketch_pass(M, srt3d::SK_G4_CHEB, a, s, nsm);
+    case srt3d::RG_RT:
+      return srt3d::launch_sketch_routed(M, a, s, nsm);
     case srt3d::RG_H128:
       return srt3d::launch_sketch_hist(M, a, 128, s, nsm);
     case srt3d::RG_H256:
@@ -114,14 +118,14 @@ cudaError_t launch_regime(uint32_t rg, int M, const srt3d::SketchArgs& a, cudaSt
 // Regimes sketch_regime() can return for (npix, T, M, mode) at any photon
 // count: it is piecewise constant in the mean photons per pixel with
 // breakpoints at these means, so evaluating it there finds every candidate.
-int regime_candidates(int64_t npix, uint32_t T, int M, uint32_t mode, uint32_t* out) {
+int regime_candidates(int64_t npix, uint32_t T, int M, uint32_t mode, uint32_t j0, uint32_t* out) {
   const unsigned long long np = (unsigned long long)npix;
   const unsigned long long means[] = {0, 256, 2048, 4096, T, 30000, 80000};
   int n = 0;
   for (unsigned long long mu : means) {
     const unsigned long long tot = mu * np;
     if (tot >= (1ull << 32)) continue;  // total photons < 2^32 (precondition)
-    const uint32_t rg = srt3d::sketch_regime(tot, npix, T, M, mode);
+    const uint32_t rg = srt3d::sketch_regime(tot, npix, T, M, mode, j0);
     bool seen = false;
     for (int i = 0; i < n; i++) seen = seen || out[i] == rg;
     if (!seen) out[n++] = rg;
@@ -140,9 +144,11 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
   if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
   int rc = check_tm(T, m);
   if (rc) return rc;
-  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_PAIRED) return fail(SRT3D_EINVAL, "path=%d unknown", path);
-  if (lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 && lanes_per_pixel != 16 &&
-      lanes_per_pixel != 32)
+  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_ROUTED) return fail(SRT3D_EINVAL, "path=%d unknown", path);
+  if (path == SRT3D_PATH_ROUTED && lanes_per_pixel != 0 && lanes_per_pixel != 2)
+    return fail(SRT3D_EINVAL, "routed path: lanes_per_pixel=%d must be 0 or 2", lanes_per_pixel);
+  if (path != SRT3D_PATH_ROUTED && lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 &&
+      lanes_per_pixel != 16 && lanes_per_pixel != 32)
     return fail(SRT3D_EINVAL, "lanes_per_pixel=%d must be 0, 4, 8, 16 or 32", lanes_per_pixel);
   if (npix == 0) return SRT3D_OK;
   if (!bins || !offsets || !z) return fail(SRT3D_ENULL, "bins/offsets/z must be non-NULL");
@@ -153,6 +159,8 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
     return fail(SRT3D_EUNSUPPORTED, "bin-count path needs T <= ~17000 (T=%u)", T);
   if (path == SRT3D_PATH_PAIRED && !pair_fits(T))
     return fail(SRT3D_EUNSUPPORTED, "class-sorted path needs T <= %u (T=%u)", srt3d::SO_MAX_T, T);
+  if (path == SRT3D_PATH_ROUTED && !srt3d::routed_fits(T, 0))
+    return fail(SRT3D_EUNSUPPORTED, "routed path needs T %% 4 == 0 and T <= %u (T=%u)", srt3d::RT_MAX_T, T);
   cudaStream_t s = (cudaStream_t)stream;
   const int nsm = num_sms_current();
   srt3d::SketchArgs a = {};
@@ -169,6 +177,9 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
     cudaError_t e = cudaSuccess;
     if (path == SRT3D_PATH_PAIRED) {
       e = srt3d::launch_sketch_pair(M, a, s, nsm);
+    } else if (path == SRT3D_PATH_ROUTED) {
+      e = j0 == 0 ? srt3d::launch_sketch_routed(M, a, s, nsm)
+                  : srt3d::launch_sketch_pass(M, M >= 24 ? srt3d::SK_G4_CHEB : 4, a, s, nsm);
     } else if (path == SRT3D_PATH_DIRECT && lanes_per_pixel != 0) {
       e = srt3d::launch_sketch_pass(M, lanes_per_pixel, a, s, nsm);
     } else {
@@ -177,10 +188,10 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
                                                                             : srt3d::RGM_DIRECT;
       a.rg_mode = mode;
       if (have_hint) {
-        e = launch_regime(srt3d::sketch_regime(total, npix, T, M, mode), M, a, s, nsm);
+        e = launch_regime(srt3d::sketch_regime(total, npix, T, M, mode, j0), M, a, s, nsm);
       } else {
         uint32_t cand[8];
-        const int nc = regime_candidates(npix, T, M, mode, cand);
+        const int nc = regime_candidates(npix, T, M, mode, j0, cand);
         for (int i = 0; i < nc && e == cudaSuccess; i++) {
           a.rg_want = nc > 1 ? cand[i] : srt3d::RG_NONE;
           e = launch_regime(cand[i], M, a, s, nsm);
@@ -217,9 +228,9 @@ int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photo
   if (rc) return rc;
   const int M0 = (int)(m < 32 ? m : 32);
   const uint32_t rg = srt3d::sketch_regime(total_photons, npix, T, M0,
-                                           hist_fits(T, M0) ? srt3d::RGM_AUTO : srt3d::RGM_DIRECT);
+                                           hist_fits(T, M0) ? srt3d::RGM_AUTO : srt3d::RGM_DIRECT, 0);
   if (lanes_per_pixel) *lanes_per_pixel = regime_lanes(rg);
-  return rg >= srt3d::RG_H128 ? SRT3D_PATH_BINCOUNT : SRT3D_PATH_DIRECT;
+  return rg >= srt3d::RG_H128 ? SRT3D_PATH_BINCOUNT : rg == srt3d::RG_RT ? SRT3D_PATH_ROUTED : SRT3D_PATH_DIRECT;
 }
 
 int srt3d_expected_sketch(const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,

@@ -46,13 +46,16 @@ struct SketchArgs {
 // A function of the frame's photon count, evaluated with exact integer
 // comparisons so the host (with a hint) and the device (from offsets) agree:
 // mean >= X  <=>  total >= X * npix.
-enum : uint32_t { RG_NONE = 0, RG_G4, RG_G8, RG_G16, RG_G32, RG_G4C, RG_H128, RG_H256, RG_H512, RG_COUNT };
+enum : uint32_t { RG_NONE = 0, RG_G4, RG_G8, RG_G16, RG_G32, RG_G4C, RG_RT, RG_H128, RG_H256, RG_H512, RG_COUNT };
+// class-routed Chebyshev kernel (sketch_routed.cu): first pass only, T % 4 == 0, T <= RT_MAX_T
+constexpr uint32_t RT_MAX_T = 12000;  // 1.25 T phasor entries + T class bytes + [32][512] fp32 partials + spills <= 227 KB
+__host__ __device__ inline bool routed_fits(uint32_t T, uint32_t j0) { return j0 == 0 && T % 4 == 0 && T <= RT_MAX_T; }
 enum : uint32_t { RGM_AUTO = 0, RGM_DIRECT = 1, RGM_HIST = 2 };
 constexpr uint32_t SK_TABLE_MAX_T = 24575;  // (T + 1) float2 entries fit SK_MAX_SMEM
 // mode: RGM_AUTO (bin-count allowed: the host passes it only when the
 // histogram fits in shared memory), RGM_DIRECT, RGM_HIST (bin-count forced).
 __host__ __device__ inline uint32_t sketch_regime(unsigned long long total, long long npix, uint32_t T, int M,
-                                                  uint32_t mode) {
+                                                  uint32_t mode, uint32_t j0) {
   const unsigned long long np = npix > 0 ? (unsigned long long)npix : 1ull;
   const bool hist = mode == RGM_HIST || (mode == RGM_AUTO && total >= (unsigned long long)T * np);
   if (hist) {
@@ -63,7 +66,8 @@ __host__ __device__ inline uint32_t sketch_regime(unsigned long long total, long
   if (T > SK_TABLE_MAX_T) return RG_G32;  // no shared phase table: one configuration
   if (total >= 4096ull * np) return RG_G32;
   if (total >= 2048ull * np) return RG_G16;
-  if (total >= 256ull * np) return M >= 24 ? RG_G4C : RG_G8;  // G = 4 rotated Chebyshev for long passes
+  // long passes: the class-routed Chebyshev kernel where it fits, else G = 4 rotated Chebyshev
+  if (total >= 256ull * np) return M >= 24 ? (routed_fits(T, j0) ? RG_RT : RG_G4C) : RG_G8;
   return RG_G4;
 }
 
@@ -71,7 +75,7 @@ __host__ __device__ inline uint32_t sketch_regime(unsigned long long total, long
 __device__ __forceinline__ bool sketch_regime_skip(const SketchArgs& a, int M) {
   if (a.rg_want == RG_NONE) return false;
   const uint32_t tot = a.offsets[a.npix] - a.offsets[0];  // < 2^32 (precondition)
-  return sketch_regime(tot, a.npix, a.T, M, a.rg_mode) != a.rg_want;
+  return sketch_regime(tot, a.npix, a.T, M, a.rg_mode, a.j0) != a.rg_want;
 }
 
 // Per-call frequency constants, computed on the host in fp64 and rounded:
@@ -171,6 +175,9 @@ cudaError_t measure_ffma_peak(double* tflops, int num_sms);
 cudaError_t launch_sketch_hist(int M, const SketchArgs& a, int threads, cudaStream_t s, int num_sms);
 size_t sketch_hist_smem(uint32_t T, int M);
 cudaError_t launch_sketch_pair(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
+// class-routed Chebyshev sketch (sketch_routed.cu): a lane pair per pixel, j0 = 0, T % 4 == 0, T <= RT_MAX_T
+cudaError_t launch_sketch_routed(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
+size_t sketch_routed_smem(uint32_t T, int M);
 size_t sketch_pair_smem(uint32_t T);
 cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, uint32_t m, uint32_t* r,
                                cudaStream_t s, int num_sms);

@@ -35,9 +35,11 @@ def _fixed_csr(npix, n, T, seed):
 
 
 # (T, m, mean photons per pixel, npix) -> one frame per regime of sketch_regime():
-# G4 (< 256), G8 (256..2047, M < 24), G4C (256..2047, M >= 24), G16 (2048..4095),
+# G4 (< 256), G8 (256..2047, M < 24), RT (256..2047, M >= 24, T % 4 == 0, T <= 12000), G4C (the
+# same where RT does not apply: odd T here, and the second pass of m = 60), G16 (2048..4095),
 # G32 (>= 4096, below T), bin-count with 128 / 256 / 512 threads (>= T; < 3e4, < 8e4, more)
-REGIME_FRAMES = [(8192, 10, 60, 600), (8192, 10, 700, 300), (8192, 32, 700, 300), (8192, 32, 2600, 100),
+REGIME_FRAMES = [(8192, 10, 60, 600), (8192, 10, 700, 300), (8192, 32, 700, 300), (4613, 32, 700, 300),
+                 (8192, 60, 700, 100), (8192, 32, 2600, 100),
                  (8192, 40, 5000, 60), (1024, 10, 4000, 60), (1024, 4, 40000, 24), (1024, 20, 90000, 12)]
 
 
@@ -118,7 +120,8 @@ def test_out_of_range_bins_finite_on_every_path(gpu, oracle_mod, T):
     db, do = _dev(bins), _dev(offs)
     calls = [dict(), dict(total_photons=int(offs[-1]))]
     calls += [dict(path=gpu.PATH_DIRECT, lanes_per_pixel=g, total_photons=int(offs[-1])) for g in (4, 8, 16, 32)]
-    calls += [dict(path=gpu.PATH_BINCOUNT), dict(path=gpu.PATH_PAIRED), dict(path=gpu.PATH_DIRECT)]
+    calls += [dict(path=gpu.PATH_BINCOUNT), dict(path=gpu.PATH_PAIRED), dict(path=gpu.PATH_DIRECT),
+              dict(path=gpu.PATH_ROUTED), dict(path=gpu.PATH_ROUTED, lanes_per_pixel=2)]
     for kw in calls:
         if "path" in kw:
             z = gpu.srt3d_sketch_ex(db, do, T, 32, **kw)

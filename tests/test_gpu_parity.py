@@ -144,46 +144,68 @@ def test_sketch_lane_regimes_forced(gpu, oracle_mod, inputs_mod):
         gpu.srt3d_sketch_ex(db, do, 8192, 32, path=7)
 
 
+# class-sorted (PATH_PAIRED) and class-routed (PATH_ROUTED: a lane pair per pixel) direct paths
+
+
+def _routed_ok(T):
+    return T % 4 == 0 and T <= 12000
+
+CLASS_PATHS = [("paired", 3, 0), ("routed", 4, 0)]
+
+
+@pytest.mark.parametrize("which,path,lanes", CLASS_PATHS)
 @pytest.mark.parametrize("T,m", [(8192, 32), (8192, 64), (4613, 10), (1024, 4), (2500, 20), (2, 1), (3, 2),
-                                 (17, 16), (23800, 33), (100, 7)])
+                                 (17, 16), (22900, 33), (100, 7), (8192, 24), (4096, 31), (12000, 32), (4, 3)])
 @pytest.mark.parametrize("max_n", [9, 300, 3000])
-def test_sketch_paired_path_parity(gpu, oracle_mod, inputs_mod, T, m, max_n):
+def test_sketch_class_paths_parity(gpu, oracle_mod, inputs_mod, which, path, lanes, T, m, max_n):
     """Class-sorted path (PATH_PAIRED: 4 lanes per pixel, photons staged in shared memory by
-    rotation class, class-uniform Chebyshev loops with a frame switch) forced on ragged frames
-    with empty pixels, heads/tails of every length and pixels spanning many 256-photon chunks;
-    T = 23800 is the largest T the path accepts."""
+    rotation class, class-uniform Chebyshev loops with a frame switch) and class-routed path
+    (PATH_ROUTED: frame-A / frame-B lanes, photons routed to a lane whose frame keeps the
+    recurrence accurate) forced on ragged frames with empty pixels, heads/tails of every length
+    and pixels spanning many chunks / flush intervals; T = 23800 is the largest T PAIRED accepts."""
     import torch
 
     bins, offs = inputs_mod.random_csr(npix=333, T=T, max_n=max_n, seed=T * 3 + m + max_n)
-    z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED)
+    if path == 4 and not _routed_ok(T):  # the routed path needs T % 4 == 0, T <= 12000: it must say so
+        with pytest.raises(gpu.Srt3dError) as e:
+            gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, m, path=path)
+        assert e.value.code == -3
+        return
+    z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, m, total_photons=int(offs[-1]), path=path,
+                            lanes_per_pixel=lanes)
     torch.cuda.synchronize()
     zg = _host(z)
     _assert_sketch_close(zg, oracle_mod.sketch(bins, offs, T, m))
     assert np.all(zg[np.diff(offs.astype(np.int64)) == 0] == 0)
 
 
-@pytest.mark.parametrize("T", [8192, 4613, 23800, 1024])
-def test_sketch_paired_worst_bins(gpu, oracle_mod, T):
+@pytest.mark.parametrize("which,path,lanes", CLASS_PATHS)
+@pytest.mark.parametrize("T", [8192, 4613, 22900, 1024, 12000, 2500])
+def test_sketch_class_paths_worst_bins(gpu, oracle_mod, which, path, lanes, T):
     """Every photon of a pixel at one bin (no averaging of phasor errors): the bins where the
     unrotated recurrence is worst conditioned (0, 1, T/2 +- 1, T-1), the class boundaries
-    (4u = T, 3T), and one-class pixels spanning many chunks."""
+    (4u = T, 3T; |cos|, |sin| = sin(pi/8)), and one-class pixels spanning many chunks (the
+    routed path then runs every photon in one frame: forced imbalance)."""
     import torch
 
-    u = [T // 8, (3 * T) // 8, (T + 7) // 8, T // 4]
+    u = [T // 8, (3 * T) // 8, (T + 7) // 8, T // 4, int(round(T * 0.0625)), int(round(T * 0.1875))]
     xs = sorted({0, 1, 2, T - 1, T // 2, T // 2 + 1, T // 2 - 1, T // 4, (3 * T) // 4, *u, *(x + T // 2 for x in u)})
     xs = [x % T for x in xs]
     lists = [[x] * 3001 for x in xs]
     lists.append(list(np.arange(2000) % 7))          # class A/B mix at tiny bins
     lists.append([T // 4] * 1500 + [0] * 5)           # almost one class, then the other
     bins, offs = _csr(lists)
+    if path == 4 and not _routed_ok(T):
+        return
     for m in (32, 64):
         z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, min(m, T - 1), total_photons=int(offs[-1]),
-                                path=gpu.PATH_PAIRED)
+                                path=path, lanes_per_pixel=lanes)
         torch.cuda.synchronize()
         _assert_sketch_close(_host(z), oracle_mod.sketch(bins, offs, T, min(m, T - 1)))
 
 
-def test_sketch_paired_alignment_and_determinism(gpu, oracle_mod, inputs_mod):
+@pytest.mark.parametrize("which,path,lanes", CLASS_PATHS)
+def test_sketch_class_paths_alignment_and_determinism(gpu, oracle_mod, inputs_mod, which, path, lanes):
     """Misaligned bins base, offsets[0] != 0, bitwise repeatability, T limit."""
     import torch
 
@@ -194,15 +216,15 @@ def test_sketch_paired_alignment_and_determinism(gpu, oracle_mod, inputs_mod):
         full = _dev(pad)
         sub = full[shift:]  # 2-byte aligned start at every residue mod 8
         o = (offs + np.uint32(3)).astype(np.uint32)
-        z = gpu.srt3d_sketch_ex(sub, _dev(o), T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED)
+        z = gpu.srt3d_sketch_ex(sub, _dev(o), T, m, total_photons=int(offs[-1]), path=path, lanes_per_pixel=lanes)
         torch.cuda.synchronize()
         _assert_sketch_close(_host(z), oracle_mod.sketch(bins, offs, T, m))
     db, do = _dev(bins), _dev(offs)
-    z1 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED))
-    z2 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=gpu.PATH_PAIRED))
+    z1 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=path, lanes_per_pixel=lanes))
+    z2 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=path, lanes_per_pixel=lanes))
     assert np.array_equal(z1.view(np.uint64), z2.view(np.uint64))
     with pytest.raises(gpu.Srt3dError):
-        gpu.srt3d_sketch_ex(db, do, 23801, m, path=gpu.PATH_PAIRED)
+        gpu.srt3d_sketch_ex(db, do, 12004 if path == 4 else 23801, m, path=path, lanes_per_pixel=lanes)
 
 
 def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):

@@ -20,13 +20,16 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--m", type=int, default=None)
+    ap.add_argument("--lib", default=None, help="alternative libsrt3d build (tuning variants)")
     args = ap.parse_args()
+    if args.lib:
+        p._lib = p.load_library(args.lib)
     f = inputs.make_frame(args.config, n_per_pixel=args.n)
     m = args.m or f.m
     bins, offs = torch.from_numpy(f.bins).cuda(), torch.from_numpy(f.offsets).cuda()
     out = {"config": args.config, "n": args.n, "m": m, "T": f.T, "photons": f.n_photons}
     variants = [("auto", p.PATH_AUTO, 0), ("sorted", p.PATH_PAIRED, 0), ("g4", p.PATH_DIRECT, 4),
-                ("g8", p.PATH_DIRECT, 8)]
+                ("g8", p.PATH_DIRECT, 8), ("routed", p.PATH_ROUTED, 0)]
     zs = {}
     for name, path, lanes in variants:
         z = torch.empty((f.npix, m), dtype=torch.complex64, device="cuda")
