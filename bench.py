@@ -56,6 +56,11 @@ def parse():
     ap.add_argument("--init-grid", type=int, default=0, help="backprojection grid points (default 16 m)")
     ap.add_argument("--init-min-sep", type=int, default=50, help="minimum separation of initial depths (bins)")
     ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 bucketing / merge timings")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the per-config sketch / gradient sweep (C1-C3, C4@1e2..1e6; SURVEY §8(d))")
+    ap.add_argument("--sweep-configs", default="C4@1e6,C1,C2,C3,C4@1e2,C4@1e3,C4@1e4,C4@1e5",
+                    help="comma list of sweep workloads (C4@<n> = C4 at n photons/pixel)")
+    ap.add_argument("--sketch-reps", type=int, default=20, help="timed sketch reps per workload (5 at C4@1e6)")
     args = ap.parse_args()
     if args.e2e_steps is None:
         args.e2e_steps = args.steps
@@ -237,6 +242,142 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------ timing helpers
+def _l2_flush(torch, buf, sink, s):
+    """Evict L2 by READING a buffer of twice its size (clean lines: no write-back lands on the
+    next kernel)."""
+    with torch.cuda.stream(s):
+        torch.sum(buf, dim=0, out=sink[0])
+
+
+def time_sketch(torch, srt3d, bins, offs, z, T, m, hint, reps, s, flush=None):
+    """Median / min over reps of one srt3d_sketch launch (CUDA events on s); the L2 is flushed
+    before every rep when `flush` = (buffer, sink) is given (inputs smaller than L2)."""
+    with torch.cuda.stream(s):
+        for _ in range(2):  # warm-up
+            srt3d.srt3d_sketch(bins, offs, T, m, z=z, total_photons=hint, stream=s)
+    times = []
+    for _ in range(reps):
+        if flush is not None:
+            _l2_flush(torch, flush[0], flush[1], s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            srt3d.srt3d_sketch(bins, offs, T, m, z=z, total_photons=hint, stream=s)
+            e1.record(s)
+        times.append((e0, e1))
+    s.synchronize()
+    ms = sorted(e0.elapsed_time(e1) for e0, e1 in times)
+    return statistics.median(ms), ms[0]
+
+
+def time_grad(torch, srt3d, z, t0, a0, sigma, T, m, iters, s, flush, reps=20):
+    """The fused gradient step: per-iteration time inside an `iters`-launch CUDA graph
+    (L2-warm theta; median of 5 replays) and single launches after an L2 flush (cold; median /
+    min of reps)."""
+    t, a = t0.clone(), a0.clone()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            srt3d.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        t.copy_(t0)
+        a.copy_(a0)
+        for _ in range(iters):
+            srt3d.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5, stream=s)
+    loop = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+        s.synchronize()
+        loop.append(e0.elapsed_time(e1) / iters)
+    cold = []
+    for _ in range(reps):
+        _l2_flush(torch, flush[0], flush[1], s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            srt3d.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5, stream=s)
+            e1.record(s)
+        cold.append((e0, e1))
+    s.synchronize()
+    cms = sorted(e0.elapsed_time(e1) for e0, e1 in cold)
+    del g
+    return statistics.median(loop), min(loop), statistics.median(cms), cms[0]
+
+
+def sketch_work(srt3d, npix, T, m, n_photons):
+    """Algorithmic bytes and flops of one sketch launch (SURVEY §8(d)): B = 2n + 4(npix+1) + 8 m npix;
+    F = 8 m n for the direct sum (direct / routed / paired paths), 8 m T npix for the bin-count path."""
+    path, lanes = srt3d.srt3d_sketch_plan(npix, T, m, n_photons)
+    b = 2.0 * n_photons + 4.0 * (npix + 1) + 8.0 * m * npix
+    f = 8.0 * m * (T * npix if path == srt3d.PATH_BINCOUNT else n_photons)
+    name = {srt3d.PATH_DIRECT: "direct", srt3d.PATH_PAIRED: "paired", srt3d.PATH_ROUTED: "routed"}.get(path,
+                                                                                                   "bincount")
+    return path, lanes, name, b, f
+
+
+def grad_work(npix, m, K, loss=False):
+    """Algorithmic bytes / flops of one fused no-loss gradient step: B = 8m + 16K per
+    pixel (z, theta in; theta out); F = 21Km + 7m + 3K per pixel minus the |r_j|^2 term (4 per j)
+    the no-loss step does not compute."""
+    return npix * (8.0 * m + 16.0 * K + (4.0 if loss else 0.0)), npix * (21.0 * K * m + (7.0 if loss else 3.0) * m
+                                                                        + 3.0 * K)
+
+
+def run_sweep(args, torch, srt3d, roofline, s, l2_bytes):
+    """Per-config sketch (and gradient) numbers for the workloads SURVEY §8(d) names besides the
+    headline: C4@1e6 (the second >= 70 % target: bin-count, HBM-bound), C1-C3 and the C4 sweep.
+    Each input is generated, timed and freed in turn."""
+    import srt3d_inputs
+
+    flush = (torch.ones(2 * max(l2_bytes, 1 << 20) // 4, dtype=torch.float32, device="cuda"),
+             torch.empty(1, dtype=torch.float32, device="cuda"))
+    out = {}
+    for wl in [w for w in args.sweep_configs.split(",") if w]:
+        name, n = (wl.split("@") + [None])[:2]
+        n = int(float(n)) if n else None
+        t_gen = time.perf_counter()
+        fr = srt3d_inputs.make_frame(name, n_per_pixel=n)
+        t_gen = time.perf_counter() - t_gen
+        bins = torch.from_numpy(fr.bins).cuda()
+        offs = torch.from_numpy(fr.offsets).cuda()
+        z = torch.empty((fr.npix, fr.m), dtype=torch.complex64, device="cuda")
+        path, lanes, pname, b, fl = sketch_work(srt3d, fr.npix, fr.T, fr.m, fr.n_photons)
+        small = 2 * fr.n_photons + 8 * fr.m * fr.npix < 2 * l2_bytes  # input + output could stay in L2
+        reps = 5 if fr.n_photons > 2e9 else args.sketch_reps
+        med, mn = time_sketch(torch, srt3d, bins, offs, z, fr.T, fr.m, fr.n_photons, reps, s,
+                              flush if small else None)
+        rec = {"workload": fr.name, "npix": fr.npix, "photons": fr.n_photons, "T": fr.T, "m": fr.m,
+               "generate_s": round(t_gen, 2),
+               "sketch": {"path": pname, "lanes_per_pixel": lanes, "reps": reps, "ms_median": med, "ms_min": mn,
+                          "photons_per_s_median": fr.n_photons / (med * 1e-3),
+                          "gbs_median": b / (med * 1e-3) / 1e9, "l2": "flushed before every rep" if small else
+                          "input larger than L2 (not flushed)",
+                          "roofline_median": roofline("srt3d_sketch", b, fl, med),
+                          "roofline_min": roofline("srt3d_sketch", b, fl, mn)}}
+        if fr.iters:
+            t0, a0 = (torch.from_numpy(x).cuda() for x in fr.theta0())
+            srt3d.srt3d_sketch(bins, offs, fr.T, fr.m, z=z, total_photons=fr.n_photons, stream=s)
+            gb, gf = grad_work(fr.npix, fr.m, fr.K)
+            lm, lmin, cm, cmin = time_grad(torch, srt3d, z, t0, a0, fr.sigma, fr.T, fr.m, fr.iters, s, flush)
+            rec["grad"] = {"iters_in_graph": fr.iters, "loop_ms_per_iter": lm, "loop_ms_min": lmin,
+                           "cold_ms_median": cm, "cold_ms_min": cmin,
+                           "pixel_iters_per_s_loop": fr.npix / (lm * 1e-3),
+                           "roofline_cold": roofline("srt3d_sketch_grad_step", gb, gf, cm),
+                           "roofline_loop": roofline("srt3d_sketch_grad_step", gb, gf, lm)}
+            del t0, a0
+        out[fr.name] = rec
+        del bins, offs, z, fr
+        torch.cuda.empty_cache()
+    del flush
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_srt3d(args):
     import torch
@@ -326,31 +467,18 @@ def run_srt3d(args):
                        "blocks pipelined (copy engine uploads block c+1 while block c computes) and frames "
                        "chained (frame f+1's uploads overlap frame f's last block)"}
 
-    # L2-cold per-launch time of the gradient kernel (outside the timed region):
-    # flush L2 by READING a buffer of 2x its size (leaves clean lines: no
-    # write-back traffic lands on the timed kernel), CUDA events around it.
-    grad_cold_ms = None
-    if f.iters > 0:
-        l2 = torch.cuda.get_device_properties(local).L2_cache_size
-        flush = torch.ones(2 * max(l2, 1 << 20) // 4, dtype=torch.float32, device="cuda")
-        sink = torch.empty(1, dtype=torch.float32, device="cuda")
-        tt, aa = pipe.t0.clone(), pipe.a0.clone()
-        times = []
-        with torch.cuda.stream(s):
-            for r in range(6):
-                torch.sum(flush, dim=0, out=sink[0])
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-                if pipe.fused:
-                    srt3d.srt3d_sketch_grad_step(pipe.z, tt, aa, f.sigma, f.T, f.m, 0.5)
-                else:
-                    srt3d.srt3d_sketch_grad(pipe.z, tt, aa, f.sigma, f.T, f.m, grad_t=pipe.gt, grad_alpha=pipe.ga,
-                                            want_loss=False)
-                e1.record(s)
-                times.append((e0, e1))
-        s.synchronize()
-        grad_cold_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in times[1:])
-        del flush
+    # Outside the timed region, on the same buffers: the sketch alone (median / min of
+    # --sketch-reps launches) and the gradient step in an `iters`-launch graph and as single
+    # launches after an L2 flush (the gradient's roofline fraction uses the
+    # L2-cold launch).
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = (torch.ones(2 * max(l2, 1 << 20) // 4, dtype=torch.float32, device="cuda"),
+             torch.empty(1, dtype=torch.float32, device="cuda"))
+    sk_rep = time_sketch(torch, srt3d, pipe.bins, pipe.offsets, pipe.z, f.T, f.m, f.n_photons, args.sketch_reps, s)
+    grad_rep = None
+    if f.iters > 0 and pipe.fused:
+        grad_rep = time_grad(torch, srt3d, pipe.z, pipe.t0, pipe.a0, f.sigma, f.T, f.m, f.iters, s, flush)
+    del flush
 
     # NEXT-4 streaming acquisition on this frame: the frame's photons as an
     # unsorted event stream (pixel ids shuffled on the GPU) -> CSR, and the
@@ -447,37 +575,44 @@ def run_srt3d(args):
                 "alg_flops_per_launch": flops}
 
     # sketch: B = 2n + 4(npix+1) + 8 m npix bytes; F = 8 m n (direct) or 8 m T npix (bin-count)
-    path, lanes = srt3d.srt3d_sketch_plan(f.npix, f.T, f.m, f.n_photons)
-    sk_bytes = 2.0 * f.n_photons + 4.0 * (f.npix + 1) + 8.0 * f.m * f.npix
-    direct_sum = path in (srt3d.PATH_DIRECT, srt3d.PATH_PAIRED)
-    sk_flops = 8.0 * f.m * (f.n_photons if direct_sum else f.T * f.npix)
+    path, lanes, pname, sk_bytes, sk_flops = sketch_work(srt3d, f.npix, f.T, f.m, f.n_photons)
     try:
         fp32_meas = srt3d.srt3d_debug_ffma_peak() * 1e12  # K8, measured in this run
     except Exception:  # pragma: no cover - measurement utility only
         fp32_meas = None
-    sketch = {"kernel": "srt3d_sketch",
-              "path": {srt3d.PATH_DIRECT: "direct", srt3d.PATH_PAIRED: "paired"}.get(path, "bincount"),
-              "lanes_per_pixel": lanes, "ms": sk_avg, "photons_per_s": f.n_photons / (sk_avg * 1e-3),
+    sketch = {"kernel": "srt3d_sketch", "path": pname, "lanes_per_pixel": lanes, "ms": sk_avg,
+              "ms_in_step_per_rep": sk_ms, "ms_median": sk_rep[0], "ms_min": sk_rep[1], "reps": args.sketch_reps,
+              "photons_per_s": f.n_photons / (sk_avg * 1e-3),
               "gbs": sk_bytes / (sk_avg * 1e-3) / 1e9, "frac_hbm": (sk_bytes / (sk_avg * 1e-3) / 1e9) / hbm,
               "tflops_direct_count": 8.0 * f.m * f.n_photons / (sk_avg * 1e-3) / 1e12,
               "roofline": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_avg),
+              "roofline_median": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_rep[0]),
+              "roofline_min": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_rep[1]),
               "fp32_measured_tflops": fp32_meas / 1e12 if fp32_meas else None,
               "frac_of_measured_fp32": (sk_flops / (sk_avg * 1e-3)) / fp32_meas if fp32_meas else None}
     grad = None
     if f.iters > 0:
         per_iter = it_avg / f.iters
-        # fused step per pixel-iteration: read z (8m) + t, alpha (8K); write t, alpha (8K)
-        g_bytes = f.npix * (8.0 * f.m + 16.0 * f.K) if pipe.fused else f.npix * (8.0 * f.m + 32.0 * f.K + 16.0 * f.K)
-        g_flops = f.npix * (21.0 * f.K * f.m + 7.0 * f.m + 3.0 * f.K)
+        g_bytes, g_flops = grad_work(f.npix, f.m, f.K)
+        if not pipe.fused:  # grad (with loss buffer untouched: NL) + separate update: theta read twice, grads through HBM
+            g_bytes = f.npix * (8.0 * f.m + 32.0 * f.K + 16.0 * f.K)
         kname = "srt3d_sketch_grad_step" if pipe.fused else "srt3d_sketch_grad+srt3d_descent_update"
         grad = {"kernel": kname, "ms_per_iter": per_iter, "pixel_iters_per_s": f.npix / (per_iter * 1e-3),
                 "gbs": g_bytes / (per_iter * 1e-3) / 1e9, "tflops": g_flops / (per_iter * 1e-3) / 1e12,
-                "roofline": roofline(kname, g_bytes, g_flops, per_iter),
+                "alg_work": "per pixel-iteration B = 8m + 16K bytes, F = 21Km + 3m + 3K flops (no-loss fused step: "
+                            "the |r|^2 term of SURVEY §8(d)'s 21Km + 7m + 3K is not computed)",
+                "roofline_in_loop": roofline(kname, g_bytes, g_flops, per_iter),
                 "note": "in-loop (CUDA-graph) time per iteration incl. node launch gaps; theta stays L2-resident "
-                        "across iterations, z is re-read from HBM each iteration (71 MB DRAM traffic per launch "
-                        "in the loop vs 80 MB algorithmic)",
-                "cold_l2_ms_per_launch": grad_cold_ms,
-                "cold_l2_roofline": roofline(kname, g_bytes, g_flops, grad_cold_ms) if grad_cold_ms else None}
+                        "across iterations, z is re-read from HBM every iteration"}
+        if grad_rep is not None:
+            grad.update({"loop_graph_ms_per_iter": grad_rep[0], "cold_l2_ms_per_launch": grad_rep[2],
+                         "cold_l2_ms_min": grad_rep[3],
+                         "cold_l2_note": "single launch after an L2 flush that READS 2x L2 (clean lines), CUDA "
+                                         "events around the launch (includes its launch latency); median / min of 20",
+                         "roofline": roofline(kname, g_bytes, g_flops, grad_rep[2]),
+                         "roofline_cold_min": roofline(kname, g_bytes, g_flops, grad_rep[3])})
+        else:
+            grad["roofline"] = grad["roofline_in_loop"]
     init = None
     if init_ms is not None:
         # backprojection + picks: F = 8 m N per pixel (one complex multiply-add per (grid point, l));
@@ -540,7 +675,10 @@ def run_srt3d(args):
                   "sketch_merge": {"kernel": "srt3d_sketch_merge", "ms": stream_ms["merge_ms"],
                                    "roofline": roofline("srt3d_sketch_merge", m_b, 0.0, stream_ms["merge_ms"])},
                   "note": "NEXT-4, timed outside the step"}
-    # dominant kernel (larger share of the step) -> the line's roofline object
+    # dominant kernel (larger share of the step) -> the line's roofline object.  The gradient's
+    # headline fraction is its L2-cold launch; the in-loop fraction rides along.
+    # `traffic` is the DRAM bytes per launch of an ncu --set full capture of the same kernel and
+    # config (profiles/traffic.json; a captured profile, not this run: ncu cannot run inside the bench).
     traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -554,6 +692,15 @@ def run_srt3d(args):
         roof = dict(grad["roofline"])
         roof["traffic"] = traffic.get("srt3d_sketch_grad_step")
         roof["share_of_step"] = it_avg / (sk_avg + it_avg)
+        roof["frac_in_loop"] = grad["roofline_in_loop"]["frac"]
+        roof["timing"] = "frac: L2-cold single launch (median of 20, events); frac_in_loop: per iteration of the step"
+    roof["traffic_source"] = "profiles/traffic.json (ncu --set full capture, DRAM read+write bytes per launch)"
+    launches = pipe.launches_per_step * args.steps
+    sweep = None
+    if not args.no_sweep and world == 1:
+        del pipe  # free the headline frame's buffers (the C4@1e6 input alone is 8.2 GB)
+        torch.cuda.empty_cache()
+        sweep = run_sweep(args, torch, srt3d, roofline, torch.cuda.Stream(), l2)
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -567,9 +714,9 @@ def run_srt3d(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Eq. (1) photon frames; stand-in for the paper's head/camouflage datasets)",
             "config": config_obj(f, args), "clocks": clocks, "e2e": e2e,
-            "gpu_launches": pipe.launches_per_step * args.steps,
+            "gpu_launches": launches,
             "roofline": roof, "cpu_baseline": cpu, "sketch": sketch, "grad": grad, "fit": fit, "init": init,
-            "stream": stream,
+            "stream": stream, "sweep": sweep,
             "step_definition": "srt3d_sketch over the frame + iters x srt3d_sketch_grad_step (CUDA graphs)"}
     print(json.dumps(line), flush=True)
     if world > 1:

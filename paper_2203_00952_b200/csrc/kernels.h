@@ -18,7 +18,7 @@ constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 #define GRAD_THREADS 64                          // gradient-kernel CTA size (one warp = 32 pixels)
 #endif
 #ifndef GRAD_TMA_MIN_BLOCKS
-#define GRAD_TMA_MIN_BLOCKS 10                   // TMA variant: swizzled addressing needs a few more registers
+#define GRAD_TMA_MIN_BLOCKS 10                   // TMA variant: 96 registers (12 measured slower in loop: tools/grad_probe.py)
 #endif
 #ifndef GRAD_MIN_BLOCKS
 #define GRAD_MIN_BLOCKS 12                       // smem caps residency at 12 CTAs/SM: let ptxas use up to 80 regs

@@ -13,7 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_bench_json_line_c1():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C1", "--steps", "3",
-                          "--warmup", "3", "--cpu-seconds", "0.5"], capture_output=True, text=True, timeout=900,
+                          "--warmup", "3", "--cpu-seconds", "0.5",
+                          "--sweep-configs", "C1,C4@1e3"], capture_output=True, text=True, timeout=900,
                          cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -31,3 +32,11 @@ def test_bench_json_line_c1():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["config"]["workload"].startswith("C1")
+    sw = d["sweep"]  # per-config sketch / gradient numbers: median, min, rooflines
+    assert set(sw) == {"C1", "C4@1e3"}
+    for rec in sw.values():
+        k = rec["sketch"]
+        assert 0 < k["ms_min"] <= k["ms_median"] and k["reps"] >= 20 and k["roofline_median"]["frac"] > 0
+    g = sw["C1"]["grad"]
+    assert 0 < g["cold_ms_min"] <= g["cold_ms_median"] and g["roofline_cold"]["frac"] > 0
+    assert "grad" not in sw["C4@1e3"]  # C4 is a sketch-only sweep

@@ -1,0 +1,92 @@
+"""Time the fused gradient step (srt3d_sketch_grad_step, the kernel the bench's
+iteration loop runs) on a C5-shaped frame (tools only): in a 200-iteration
+CUDA graph (L2-warm theta) and as single launches after an L2 flush (cold),
+median / min over reps.  z is the expected sketch of a random theta* plus
+noise (the kernel's cost does not depend on the values).
+
+  python tools/grad_probe.py [--npix 262144] [--m 32] [--K 3] [--lib other.so]"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2203_00952_b200 as p  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--npix", type=int, default=512 * 512)
+    ap.add_argument("--m", type=int, default=32)
+    ap.add_argument("--K", type=int, default=3)
+    ap.add_argument("--T", type=int, default=8192)
+    ap.add_argument("--sigma", type=float, default=6.0)
+    ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--lib", default=None)
+    a = ap.parse_args()
+    if a.lib:
+        p._lib = p.load_library(a.lib)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    t = torch.rand((a.npix, a.K), device="cuda", generator=g) * a.T
+    al = torch.rand((a.npix, a.K), device="cuda", generator=g) * 0.9 + 0.05
+    z = p.srt3d_expected_sketch(t, al, a.sigma, a.T, a.m)
+    z += 0.01 * torch.randn(z.shape, dtype=torch.complex64, device="cuda", generator=g)
+    t0, a0 = t + 10.0, al.clone()
+    tt, aa = t0.clone(), a0.clone()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        tt.copy_(t0)
+        aa.copy_(a0)
+        for _ in range(a.iters):
+            p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+    loop = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            graph.replay()
+            e1.record(s)
+        s.synchronize()
+        loop.append(e0.elapsed_time(e1) * 1000.0 / a.iters)
+    flush = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sink = torch.empty(1, dtype=torch.float32, device="cuda")
+    cold, dirty = [], []
+    for _ in range(a.reps):  # dirty-L2 cold: the flush WRITES 512 MB (L2 full of dirty lines)
+        with torch.cuda.stream(s):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+            e1.record(s)
+        s.synchronize()
+        dirty.append(e0.elapsed_time(e1) * 1000.0)
+    for _ in range(a.reps):  # clean-L2 cold: the flush READS 512 MB (L2 full of clean lines)
+        with torch.cuda.stream(s):
+            sink.copy_(flush.sum().reshape(1))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+            e1.record(s)
+        s.synchronize()
+        cold.append(e0.elapsed_time(e1) * 1000.0)
+    loop.sort()
+    cold.sort()
+    dirty.sort()
+    nbytes = a.npix * (8 * a.m + 16 * a.K)
+    print(json.dumps({"npix": a.npix, "m": a.m, "K": a.K, "lib": a.lib, "loop_us_median": loop[len(loop) // 2],
+                      "loop_us_min": loop[0], "cold_us_median": cold[len(cold) // 2], "cold_us_min": cold[0],
+                      "dirty_cold_us_median": dirty[len(dirty) // 2], "dirty_cold_us_min": dirty[0],
+                      "cold_frac_hbm": nbytes / (cold[len(cold) // 2] * 1e-6) / 6545.3e9,
+                      "loop_frac_hbm": nbytes / (loop[len(loop) // 2] * 1e-6) / 6545.3e9}))
+
+
+if __name__ == "__main__":
+    main()
