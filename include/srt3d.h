@@ -290,7 +290,10 @@ int srt3d_sketch_accumulate(float* z, uint32_t* n, const float* zb, const uint32
  * bin) into the pixel-sorted CSR frame srt3d_sketch consumes (reading A21),
  * by a two-level counting sort with coalesced writes:
  * offsets[i] = number of events with pixel < i, offsets[npix] = kept events,
- * and each pixel's bins contiguous in bins_out.  Within a pixel the order
+ * and each pixel's bins contiguous in bins_out.  For npix <= 512 * 8192 the
+ * sort is STABLE (each pixel's bins keep their stream order): the output is
+ * deterministic, bit-identical run to run and to a stable counting sort;
+ * larger frames use a one-level atomic scatter whose within-pixel order
  * follows atomic arrival (a permutation of the stable order; the sketch is
  * order-invariant up to fp32 rounding).  Events with pixel >= npix are
  * dropped and counted into *dropped (device uint32, may be NULL).
