@@ -338,6 +338,8 @@ def run_sweep(args, torch, srt3d, roofline, s, l2_bytes):
     flush = (torch.ones(2 * max(l2_bytes, 1 << 20) // 4, dtype=torch.float32, device="cuda"),
              torch.empty(1, dtype=torch.float32, device="cuda"))
     out = {}
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for wl in [w for w in args.sweep_configs.split(",") if w]:
         name, n = (wl.split("@") + [None])[:2]
         n = int(float(n)) if n else None
@@ -359,7 +361,8 @@ def run_sweep(args, torch, srt3d, roofline, s, l2_bytes):
                           "gbs_median": b / (med * 1e-3) / 1e9, "l2": "flushed before every rep" if small else
                           "input larger than L2 (not flushed)",
                           "roofline_median": roofline("srt3d_sketch", b, fl, med),
-                          "roofline_min": roofline("srt3d_sketch", b, fl, mn)}}
+                          "roofline_min": roofline("srt3d_sketch", b, fl, mn),
+                          "traffic": traffic.get(fr.name, {}).get("srt3d_sketch")}}
         if fr.iters:
             t0, a0 = (torch.from_numpy(x).cuda() for x in fr.theta0())
             srt3d.srt3d_sketch(bins, offs, fr.T, fr.m, z=z, total_photons=fr.n_photons, stream=s)
@@ -369,7 +372,8 @@ def run_sweep(args, torch, srt3d, roofline, s, l2_bytes):
                            "cold_ms_median": cm, "cold_ms_min": cmin,
                            "pixel_iters_per_s_loop": fr.npix / (lm * 1e-3),
                            "roofline_cold": roofline("srt3d_sketch_grad_step", gb, gf, cm),
-                           "roofline_loop": roofline("srt3d_sketch_grad_step", gb, gf, lm)}
+                           "roofline_loop": roofline("srt3d_sketch_grad_step", gb, gf, lm),
+                           "traffic": traffic.get(fr.name, {}).get("srt3d_sketch_grad_step")}
             del t0, a0
         out[fr.name] = rec
         del bins, offs, z, fr
