@@ -307,7 +307,29 @@ def time_grad(torch, srt3d, z, t0, a0, sigma, T, m, iters, s, flush, reps=20):
     s.synchronize()
     cms = sorted(e0.elapsed_time(e1) for e0, e1 in cold)
     del g
-    return statistics.median(loop), min(loop), statistics.median(cms), cms[0]
+
+    # the same cold launch without its launch latency: CUDA graphs of n x [flush, step] and
+    # n x [flush], events around each replay; per-launch cold time = the difference / n
+    def graph_ms(with_step, n=10):
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=s):
+            for _ in range(n):
+                _l2_flush(torch, flush[0], flush[1], s)
+                if with_step:
+                    srt3d.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5, stream=s)
+        res = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record(s)
+                g2.replay()
+                e1.record(s)
+            s.synchronize()
+            res.append(e0.elapsed_time(e1))
+        del g2
+        return statistics.median(res) / n
+    in_graph = graph_ms(True) - graph_ms(False)
+    return statistics.median(loop), min(loop), statistics.median(cms), cms[0], in_graph
 
 
 def sketch_work(srt3d, npix, T, m, n_photons):
@@ -367,11 +389,12 @@ def run_sweep(args, torch, srt3d, roofline, s, l2_bytes):
             t0, a0 = (torch.from_numpy(x).cuda() for x in fr.theta0())
             srt3d.srt3d_sketch(bins, offs, fr.T, fr.m, z=z, total_photons=fr.n_photons, stream=s)
             gb, gf = grad_work(fr.npix, fr.m, fr.K)
-            lm, lmin, cm, cmin = time_grad(torch, srt3d, z, t0, a0, fr.sigma, fr.T, fr.m, fr.iters, s, flush)
+            lm, lmin, cm, cmin, cg = time_grad(torch, srt3d, z, t0, a0, fr.sigma, fr.T, fr.m, fr.iters, s, flush)
             rec["grad"] = {"iters_in_graph": fr.iters, "loop_ms_per_iter": lm, "loop_ms_min": lmin,
-                           "cold_ms_median": cm, "cold_ms_min": cmin,
+                           "cold_ms_in_graph": cg, "cold_single_launch_ms_median": cm, "cold_single_launch_ms_min": cmin,
                            "pixel_iters_per_s_loop": fr.npix / (lm * 1e-3),
-                           "roofline_cold": roofline("srt3d_sketch_grad_step", gb, gf, cm),
+                           "roofline_cold": roofline("srt3d_sketch_grad_step", gb, gf, cg),
+                           "roofline_cold_single_launch": roofline("srt3d_sketch_grad_step", gb, gf, cm),
                            "roofline_loop": roofline("srt3d_sketch_grad_step", gb, gf, lm),
                            "traffic": traffic.get(fr.name, {}).get("srt3d_sketch_grad_step")}
             del t0, a0
@@ -607,14 +630,18 @@ def run_srt3d(args):
                             "the |r|^2 term of SURVEY §8(d)'s 21Km + 7m + 3K is not computed)",
                 "roofline_in_loop": roofline(kname, g_bytes, g_flops, per_iter),
                 "note": "in-loop (CUDA-graph) time per iteration incl. node launch gaps; theta stays L2-resident "
-                        "across iterations, z is re-read from HBM every iteration"}
+                        "across iterations, z is re-read from HBM every iteration (single-pass ncu mid-loop: "
+                        "65.9 MB DRAM reads per launch)"}
         if grad_rep is not None:
-            grad.update({"loop_graph_ms_per_iter": grad_rep[0], "cold_l2_ms_per_launch": grad_rep[2],
-                         "cold_l2_ms_min": grad_rep[3],
-                         "cold_l2_note": "single launch after an L2 flush that READS 2x L2 (clean lines), CUDA "
-                                         "events around the launch (includes its launch latency); median / min of 20",
-                         "roofline": roofline(kname, g_bytes, g_flops, grad_rep[2]),
-                         "roofline_cold_min": roofline(kname, g_bytes, g_flops, grad_rep[3])})
+            grad.update({"loop_graph_ms_per_iter": grad_rep[0], "cold_l2_ms_per_launch": grad_rep[4],
+                         "cold_l2_single_launch_ms_median": grad_rep[2], "cold_l2_single_launch_ms_min": grad_rep[3],
+                         "cold_l2_note": "every launch after an L2 flush that READS 2x L2 (clean lines). "
+                                         "cold_l2_ms_per_launch: CUDA events around graphs of 10 x [flush, step] minus "
+                                         "10 x [flush] (the kernel without its launch latency; ncu's "
+                                         "gpu__time_duration of the same launch agrees); single_launch: events "
+                                         "around one launch (adds ~2.5 us of launch latency), median / min of 20",
+                         "roofline": roofline(kname, g_bytes, g_flops, grad_rep[4]),
+                         "roofline_cold_single_launch": roofline(kname, g_bytes, g_flops, grad_rep[2])})
         else:
             grad["roofline"] = grad["roofline_in_loop"]
     init = None
@@ -697,7 +724,8 @@ def run_srt3d(args):
         roof["traffic"] = traffic.get("srt3d_sketch_grad_step")
         roof["share_of_step"] = it_avg / (sk_avg + it_avg)
         roof["frac_in_loop"] = grad["roofline_in_loop"]["frac"]
-        roof["timing"] = "frac: L2-cold single launch (median of 20, events); frac_in_loop: per iteration of the step"
+        roof["timing"] = ("frac: L2-cold launch (events around graphs of [L2 flush, step] minus [L2 flush]); "
+                          "frac_in_loop: per iteration of the step")
     roof["traffic_source"] = "profiles/traffic.json (ncu --set full capture, DRAM read+write bytes per launch)"
     launches = pipe.launches_per_step * args.steps
     sweep = None

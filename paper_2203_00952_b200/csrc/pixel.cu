@@ -341,6 +341,12 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
   // one mbarrier per box: the j loop waits for box h only when it reaches j = 16 h,
   // so later boxes land while the first frequencies are computed
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(GRAD_THREADS / 32) * NBOX * 4096) + warp * NBOX;
+  // theta first: the phasor anchors need it before any z, and issued ahead of the z boxes it
+  // is not queued behind them in DRAM (C5 L2-cold launch 18.5 -> 17.9 us, in loop 14.0 -> 13.65 us)
+  const long long i = row0 + lane;
+  const bool active = i < a.npix;
+  float tk[K], ak[K];
+  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
   if (lane == 0) {
 #pragma unroll
     for (int h = 0; h < NBOX; h++) mbar_init(bar + h, 1);
@@ -352,10 +358,6 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
     }
   }
   __syncwarp();
-  const long long i = row0 + lane;
-  const bool active = i < a.npix;
-  float tk[K], ak[K];
-  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
   float gt[K], ga[K], L;
   pixel_body<K, M, MODE, true, true>(a, reinterpret_cast<float2*>(tile + lane * 128), nullptr, nullptr, tk, ak, gt,
                                      ga, L, bar);

@@ -77,6 +77,51 @@ def main():
             e1.record(s)
         s.synchronize()
         cold.append(e0.elapsed_time(e1) * 1000.0)
+    empty, warm1 = [], []
+    for _ in range(a.reps):  # the same clean flush, then a 1-element kernel: event + launch overhead
+        with torch.cuda.stream(s):
+            sink.copy_(flush.sum().reshape(1))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            sink.add_(1.0)
+            e1.record(s)
+        s.synchronize()
+        empty.append(e0.elapsed_time(e1) * 1000.0)
+    for _ in range(a.reps):  # a single launch right after another one (L2-warm, not in a graph)
+        with torch.cuda.stream(s):
+            p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+            e1.record(s)
+        s.synchronize()
+        warm1.append(e0.elapsed_time(e1) * 1000.0)
+    # cold per launch inside CUDA graphs (launch overhead hidden): [flush, step] x N minus [flush] x N
+    def graph_ms(with_step, n=20):
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=s):
+            for _ in range(n):
+                sink.copy_(flush.sum().reshape(1))
+                for _ in range(with_step):
+                    p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
+        res = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record(s)
+                g2.replay()
+                e1.record(s)
+            s.synchronize()
+            res.append(e0.elapsed_time(e1))
+        del g2
+        return sorted(res)[2], n
+    gw, n_g = graph_ms(1)
+    gf, _ = graph_ms(0)
+    g2w, _ = graph_ms(2)
+    graph_cold = (gw - gf) * 1000.0 / n_g
+    graph_second = (g2w - gw) * 1000.0 / n_g  # the launch right after a cold one (theta L2-warm)
+    empty.sort()
+    warm1.sort()
     loop.sort()
     cold.sort()
     dirty.sort()
@@ -84,6 +129,9 @@ def main():
     print(json.dumps({"npix": a.npix, "m": a.m, "K": a.K, "lib": a.lib, "loop_us_median": loop[len(loop) // 2],
                       "loop_us_min": loop[0], "cold_us_median": cold[len(cold) // 2], "cold_us_min": cold[0],
                       "dirty_cold_us_median": dirty[len(dirty) // 2], "dirty_cold_us_min": dirty[0],
+                      "empty_after_flush_us_median": empty[len(empty) // 2],
+                      "warm_single_us_median": warm1[len(warm1) // 2],
+                      "cold_in_graph_us": graph_cold, "second_after_cold_in_graph_us": graph_second,
                       "cold_frac_hbm": nbytes / (cold[len(cold) // 2] * 1e-6) / 6545.3e9,
                       "loop_frac_hbm": nbytes / (loop[len(loop) // 2] * 1e-6) / 6545.3e9}))
 
