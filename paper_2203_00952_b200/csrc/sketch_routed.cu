@@ -12,7 +12,7 @@
 //   frame B: phi = theta + pi/2,  accurate iff |cos theta| >= tau
 //            (e^{i j phi} = i^j e^{i j theta}: the frame-B sums are rotated
 //            back by (-i)^j once per fold),
-// tau = 0.25: worst phasor error 4.1e-6 for j <= 32 at every T tested
+// tau = 0.2: worst phasor error 4.9e-6 for j <= 32 at every T tested
 // (tools/sim_cheb_tau.c), inside the 1e-5 sketch tolerance even when every
 // photon of a pixel sits in one worst-case bin.
 //
@@ -22,7 +22,7 @@
 // e^{i theta} = tab[x], swap masks with one shuffle, and decide per slot:
 //   keep  — A-lane runs its own photon, B-lane its own;
 //   swap  — they exchange photons (the x values come with the same shuffle);
-//   clash — both photons need the same frame (5 % of slots for uniform
+//   clash — both photons need the same frame (3.3 % of slots for uniform
 //           photons): that frame's lane runs its photon, the other photon is
 //           appended to a per-pair spill list of that frame, run later.
 // So each lane runs exactly 8 photon slots per round (a clash leaves one
@@ -39,7 +39,8 @@
 
 namespace srt3d {
 
-constexpr float RT_TAU = 0.25f;           // frame accuracy threshold (tools/sim_cheb_tau.c)
+constexpr float RT_TAU = 0.2f;            // frame accuracy threshold (tools/sim_cheb_tau.c: 4.9e-6; 0.25: 4.1e-6
+                                          // but 5.2 % clash slots instead of 3.3 %)
 constexpr int RT_THREADS = 512;           // CTA size: one CTA per SM (shared memory), 16 warps
 constexpr int RT_FOLD_ROUNDS = 16;        // rounds between folds: <= 128 photon slots per lane per partial
 constexpr int RT_SPILL_CAP = 32;          // spill-list entries per lane (uint16 bins)
