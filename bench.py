@@ -212,7 +212,8 @@ def config_obj(f, args):
             "npix": f.npix, "photons_per_frame": f.n_photons, "T": f.T, "m": f.m, "K": f.K, "sigma": f.sigma,
             "iters": f.iters, "seed": f.seed, "recipe": f.recipe,
             "l2": "photon input per step larger than L2 (not flushed); in the iteration loop theta stays L2-resident "
-                  "and z streams from HBM every iteration (measured: 67 MB DRAM reads per launch)",
+                  "and z (67 MB) partly (two-z loop: 14.7 vs 13.6 us per iteration); the gradient's headline "
+                  "fraction is its L2-flushed launch",
             "parallelism": f"dp{args.gpus} (independent frames per GPU)"}
 
 
@@ -630,8 +631,9 @@ def run_srt3d(args):
                             "the |r|^2 term of SURVEY §8(d)'s 21Km + 7m + 3K is not computed)",
                 "roofline_in_loop": roofline(kname, g_bytes, g_flops, per_iter),
                 "note": "in-loop (CUDA-graph) time per iteration incl. node launch gaps; theta stays L2-resident "
-                        "across iterations, z is re-read from HBM every iteration (single-pass ncu mid-loop: "
-                        "65.9 MB DRAM reads per launch)"}
+                        "across iterations and z (67 MB) partly: the same loop alternating two copies of z "
+                        "(134 MB > L2, z always from HBM) runs 14.7 instead of 13.6 us per iteration "
+                        "(tools/grad_probe.py loop_two_z_us_median)"}
         if grad_rep is not None:
             grad.update({"loop_graph_ms_per_iter": grad_rep[0], "cold_l2_ms_per_launch": grad_rep[4],
                          "cold_l2_single_launch_ms_median": grad_rep[2], "cold_l2_single_launch_ms_min": grad_rep[3],

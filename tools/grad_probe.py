@@ -56,6 +56,24 @@ def main():
             e1.record(s)
         s.synchronize()
         loop.append(e0.elapsed_time(e1) * 1000.0 / a.iters)
+    # the loop alternating two copies of z (134 MB > L2): z cannot stay L2-resident
+    z2 = z.clone()
+    g_alt = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_alt, stream=s):
+        tt.copy_(t0)
+        aa.copy_(a0)
+        for it in range(a.iters):
+            p.srt3d_sketch_grad_step(z if it % 2 == 0 else z2, tt, aa, a.sigma, a.T, a.m, stream=s)
+    alt = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            g_alt.replay()
+            e1.record(s)
+        s.synchronize()
+        alt.append(e0.elapsed_time(e1) * 1000.0 / a.iters)
+    del g_alt
     flush = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     sink = torch.empty(1, dtype=torch.float32, device="cuda")
     cold, dirty = [], []
@@ -97,11 +115,19 @@ def main():
         s.synchronize()
         warm1.append(e0.elapsed_time(e1) * 1000.0)
     # cold per launch inside CUDA graphs (launch overhead hidden): [flush, step] x N minus [flush] x N
-    def graph_ms(with_step, n=20):
+    # one float per 2 MB page of z and theta (warms the TLBs, leaves L2 ~empty of them)
+    zf = torch.view_as_real(z).reshape(-1)
+    pages = [x[:: (2 << 20) // 4] for x in (zf, tt.reshape(-1), aa.reshape(-1))]
+    psink = torch.zeros(1, device="cuda")
+
+    def graph_ms(with_step, n=20, touch=False):
         g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g2, stream=s):
             for _ in range(n):
                 sink.copy_(flush.sum().reshape(1))
+                if touch:
+                    for pg in pages:
+                        psink.add_(pg.sum())
                 for _ in range(with_step):
                     p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
         res = []
@@ -120,6 +146,9 @@ def main():
     g2w, _ = graph_ms(2)
     graph_cold = (gw - gf) * 1000.0 / n_g
     graph_second = (g2w - gw) * 1000.0 / n_g  # the launch right after a cold one (theta L2-warm)
+    gtw, _ = graph_ms(1, touch=True)
+    gtf, _ = graph_ms(0, touch=True)
+    graph_cold_tlb = (gtw - gtf) * 1000.0 / n_g  # cold L2, TLB entries of z / theta warmed
     empty.sort()
     warm1.sort()
     loop.sort()
@@ -132,6 +161,8 @@ def main():
                       "empty_after_flush_us_median": empty[len(empty) // 2],
                       "warm_single_us_median": warm1[len(warm1) // 2],
                       "cold_in_graph_us": graph_cold, "second_after_cold_in_graph_us": graph_second,
+                      "cold_tlb_warm_in_graph_us": graph_cold_tlb,
+                      "loop_two_z_us_median": sorted(alt)[2],
                       "cold_frac_hbm": nbytes / (cold[len(cold) // 2] * 1e-6) / 6545.3e9,
                       "loop_frac_hbm": nbytes / (loop[len(loop) // 2] * 1e-6) / 6545.3e9}))
 
