@@ -311,7 +311,7 @@ def time_grad(torch, srt3d, z, t0, a0, sigma, T, m, iters, s, flush, reps=20):
 
     # the same cold launch without its launch latency: CUDA graphs of n x [flush, step] and
     # n x [flush], events around each replay; per-launch cold time = the difference / n
-    def graph_ms(with_step, n=10):
+    def graph_ms(with_step, n=20):
         g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g2, stream=s):
             for _ in range(n):
@@ -319,7 +319,7 @@ def time_grad(torch, srt3d, z, t0, a0, sigma, T, m, iters, s, flush, reps=20):
                 if with_step:
                     srt3d.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5, stream=s)
         res = []
-        for _ in range(5):
+        for _ in range(7):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(s):
                 e0.record(s)
@@ -638,8 +638,8 @@ def run_srt3d(args):
             grad.update({"loop_graph_ms_per_iter": grad_rep[0], "cold_l2_ms_per_launch": grad_rep[4],
                          "cold_l2_single_launch_ms_median": grad_rep[2], "cold_l2_single_launch_ms_min": grad_rep[3],
                          "cold_l2_note": "every launch after an L2 flush that READS 2x L2 (clean lines). "
-                                         "cold_l2_ms_per_launch: CUDA events around graphs of 10 x [flush, step] minus "
-                                         "10 x [flush] (the kernel without its launch latency; ncu's "
+                                         "cold_l2_ms_per_launch: CUDA events around graphs of 20 x [flush, step] minus "
+                                         "20 x [flush] (the kernel without its launch latency; ncu's "
                                          "gpu__time_duration of the same launch agrees); single_launch: events "
                                          "around one launch (adds ~2.5 us of launch latency), median / min of 20",
                          "roofline": roofline(kname, g_bytes, g_flops, grad_rep[4]),
