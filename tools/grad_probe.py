@@ -120,7 +120,7 @@ def main():
     pages = [x[:: (2 << 20) // 4] for x in (zf, tt.reshape(-1), aa.reshape(-1))]
     psink = torch.zeros(1, device="cuda")
 
-    def graph_ms(with_step, n=20, touch=False):
+    def graph_ms(with_step, n=20, touch=False, icache=False):
         g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g2, stream=s):
             for _ in range(n):
@@ -128,6 +128,8 @@ def main():
                 if touch:
                     for pg in pages:
                         psink.add_(pg.sum())
+                if icache:  # one 64-pixel launch of the same kernel: its code into the caches
+                    p.srt3d_sketch_grad_step(z[:64], tt[:64], aa[:64], a.sigma, a.T, a.m, stream=s)
                 for _ in range(with_step):
                     p.srt3d_sketch_grad_step(z, tt, aa, a.sigma, a.T, a.m, stream=s)
         res = []
@@ -149,6 +151,14 @@ def main():
     gtw, _ = graph_ms(1, touch=True)
     gtf, _ = graph_ms(0, touch=True)
     graph_cold_tlb = (gtw - gtf) * 1000.0 / n_g  # cold L2, TLB entries of z / theta warmed
+    pages[:] = [tt.reshape(-1), aa.reshape(-1)]  # now: read all of theta (6 MB) into L2 after the flush
+    gqw, _ = graph_ms(1, touch=True)
+    gqf, _ = graph_ms(0, touch=True)
+    graph_cold_theta_warm = (gqw - gqf) * 1000.0 / n_g
+    giw, _ = graph_ms(1, icache=True)
+    gif, _ = graph_ms(0, icache=True)
+    graph_cold_icache_warm = (giw - gif) * 1000.0 / n_g
+
     empty.sort()
     warm1.sort()
     loop.sort()
@@ -161,7 +171,8 @@ def main():
                       "empty_after_flush_us_median": empty[len(empty) // 2],
                       "warm_single_us_median": warm1[len(warm1) // 2],
                       "cold_in_graph_us": graph_cold, "second_after_cold_in_graph_us": graph_second,
-                      "cold_tlb_warm_in_graph_us": graph_cold_tlb,
+                      "cold_tlb_warm_in_graph_us": graph_cold_tlb, "cold_theta_warm_in_graph_us": graph_cold_theta_warm,
+                      "cold_code_warm_in_graph_us": graph_cold_icache_warm,
                       "loop_two_z_us_median": sorted(alt)[2],
                       "cold_frac_hbm": nbytes / (cold[len(cold) // 2] * 1e-6) / 6545.3e9,
                       "loop_frac_hbm": nbytes / (loop[len(loop) // 2] * 1e-6) / 6545.3e9}))
