@@ -20,6 +20,10 @@ constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 #ifndef GRAD_TMA_MIN_BLOCKS
 #define GRAD_TMA_MIN_BLOCKS 10                   // TMA variant: 96 registers (12 measured slower in loop: tools/grad_probe.py)
 #endif
+#ifndef GRAD_PERSIST
+#define GRAD_PERSIST 0  // 1: one wave of TMA-gradient CTAs, each warp looping over tiles (measured slower:
+                        // C5 22.4 us cold, 16.4 in loop vs 18.0 / 13.55 — per-warp tiles in sequence expose the loads)
+#endif
 #ifndef GRAD_MIN_BLOCKS
 #define GRAD_MIN_BLOCKS 12                       // smem caps residency at 12 CTAs/SM: let ptxas use up to 80 regs
 #endif

@@ -149,7 +149,8 @@ __device__ __forceinline__ void load_theta(const PixArgs& a, long long i, float 
 template <int K, int M, int MODE, bool WAIT_Z = true, bool ZTMA = false>
 __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const float* s_hh, const float* s_wh,
                                            const float (&tk)[K], const float (&ak)[K], float (&gt)[K],
-                                           float (&ga)[K], float& L, uint64_t* zbar = nullptr) {
+                                           float (&ga)[K], float& L, uint64_t* zbar = nullptr,
+                                           uint32_t zpar = 0u) {
   const int m = M ? M : (int)a.m;
   uint32_t q[K];
   u64 W[K], Wn[K], P[K];
@@ -165,7 +166,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
   if (MODE != PX_EXPECTED && WAIT_Z) {
     // the anchors above overlap the z slab's copy; wait for it only now
     if (ZTMA) {
-      mbar_wait(zbar, 0);  // box 0 (j < 16); later boxes are awaited inside the j loop
+      mbar_wait(zbar, zpar);  // box 0 (j < 16); later boxes are awaited inside the j loop
     } else {
       cp_async_wait_all();
       __syncwarp();
@@ -181,7 +182,7 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
 
 #pragma unroll(M ? M : 1)
   for (int j = 0; j < m; j++) {  // frequency j+1
-    if (ZTMA && MODE != PX_EXPECTED && WAIT_Z && j > 0 && j % 16 == 0) mbar_wait(zbar + j / 16, 0);
+    if (ZTMA && MODE != PX_EXPECTED && WAIT_Z && j > 0 && j % 16 == 0) mbar_wait(zbar + j / 16, zpar);
     if (j > 0) {
       if ((j & 31) == 0) {
 #pragma unroll
@@ -335,33 +336,42 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
   extern __shared__ unsigned char tma_smem_raw[];
   unsigned char* smem = tma_smem_raw + ((1024u - (smem_u32(tma_smem_raw) & 1023u)) & 1023u);  // 1 KB aligned
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5);
-  if (row0 >= a.npix) return;
   unsigned char* tile = smem + (size_t)warp * NBOX * 4096;
   // one mbarrier per box: the j loop waits for box h only when it reaches j = 16 h,
   // so later boxes land while the first frequencies are computed
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(GRAD_THREADS / 32) * NBOX * 4096) + warp * NBOX;
-  // theta first: the phasor anchors need it before any z, and issued ahead of the z boxes it
-  // is not queued behind them in DRAM (C5 L2-cold launch 18.5 -> 17.9 us, in loop 14.0 -> 13.65 us)
-  const long long i = row0 + lane;
-  const bool active = i < a.npix;
-  float tk[K], ak[K];
-  load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
   if (lane == 0) {
 #pragma unroll
     for (int h = 0; h < NBOX; h++) mbar_init(bar + h, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#pragma unroll
-    for (int h = 0; h < NBOX; h++) {
-      mbar_expect_tx(bar + h, 4096u);
-      tma_load_2d(tile + h * 4096, &tm, h * 32, (int)row0, bar + h);
-    }
   }
   __syncwarp();
-  float gt[K], ga[K], L;
-  pixel_body<K, M, MODE, true, true>(a, reinterpret_cast<float2*>(tile + lane * 128), nullptr, nullptr, tk, ak, gt,
-                                     ga, L, bar);
-  if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
+  uint32_t par = 0u;
+  // GRAD_PERSIST: one wave of CTAs, each warp loops over its 32-row tiles; else one tile per warp
+  for (long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5); row0 < a.npix;
+       row0 += GRAD_PERSIST ? (long long)gridDim.x * blockDim.x : a.npix) {
+    // theta first: the phasor anchors need it before any z, and issued ahead of the z boxes it
+    // is not queued behind them in DRAM (C5 L2-cold launch 18.5 -> 17.9 us, in loop 14.0 -> 13.65 us)
+    const long long i = row0 + lane;
+    const bool active = i < a.npix;
+    float tk[K], ak[K];
+    load_theta<K>(a, active ? i : a.npix - 1, tk, ak);
+    if (lane == 0) {
+#pragma unroll
+      for (int h = 0; h < NBOX; h++) {
+        mbar_expect_tx(bar + h, 4096u);
+        tma_load_2d(tile + h * 4096, &tm, h * 32, (int)row0, bar + h);
+      }
+    }
+    __syncwarp();
+    float gt[K], ga[K], L;
+    pixel_body<K, M, MODE, true, true>(a, reinterpret_cast<float2*>(tile + lane * 128), nullptr, nullptr, tk, ak, gt,
+                                       ga, L, bar, par);
+    if (active) pixel_store<K, MODE>(a, i, tk, ak, gt, ga, L);
+    par ^= 1u;
+    __syncwarp();  // every lane has read the tile before the next boxes overwrite it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (static cudart).
@@ -534,7 +544,15 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
           static SmemAttrOnce tattr;
           cudaError_t e = smem_attr_once(tattr, tfn, (int)tsmem);
           if (e != cudaSuccess) return e;
-          const long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
+          long long grid = (a.npix + GRAD_THREADS - 1) / GRAD_THREADS;
+          if (GRAD_PERSIST) {  // one wave
+            static OccCache tocc;
+            int per_sm = 0;
+            e = occupancy_cached(tocc, tfn, GRAD_THREADS, tsmem, &per_sm);
+            if (e != cudaSuccess) return e;
+            const long long wave = (long long)per_sm * num_sms_device();
+            if (wave > 0 && grid > wave) grid = wave;
+          }
           tfn<<<(unsigned)grid, GRAD_THREADS, tsmem, s>>>(a, tm);
           return cudaGetLastError();
         }
