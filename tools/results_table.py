@@ -12,7 +12,7 @@ RUNS = [("C1", None), ("C2", None), ("C3", None), ("C5", None)] + [("C4", n) for
 
 def run(cfg, n):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "5", "--warmup", "3",
-           "--no-e2e", "--no-init", "--no-stream", "--cpu-seconds", "6"]  # (fit: timed by default)
+           "--no-e2e", "--no-init", "--no-stream", "--no-sweep", "--cpu-seconds", "6"]  # (fit: timed by default)
     if n:
         cmd += ["--n-per-pixel", str(n)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
@@ -36,10 +36,11 @@ def main():
                     f"| {name} | sketch ({sk['path']}) | {sk['ms']:.4f} ms | {sk['photons_per_s']:.3g} photons/s | "
                     f"{sk['gbs']:.0f} | {100 * rf['frac']:.1f} % ({rf['bound']}) | {clk} MHz | – | – | ≤1e-5 (tests) |")
         if g:
-            gr = g["roofline"]
-            rows.append(f"| {name} | gradient step (in loop) | {1000 * g['ms_per_iter']:.2f} µs/iter | "
-                        f"{g['pixel_iters_per_s']:.3g} px-it/s | {g['gbs']:.0f} | {100 * gr['frac']:.1f} % "
-                        f"({gr['bound']}; cold {100 * g['cold_l2_roofline']['frac']:.0f} %) | {clk} MHz | "
+            gr, gc = g["roofline_in_loop"], g["roofline"]
+            rows.append(f"| {name} | gradient step (in loop; L2-cold launch) | {1000 * g['ms_per_iter']:.2f} µs/iter; "
+                        f"{1000 * g['cold_l2_ms_per_launch']:.2f} µs | "
+                        f"{g['pixel_iters_per_s']:.3g} px-it/s | {g['gbs']:.0f} | {100 * gr['frac']:.1f} %; cold "
+                        f"{100 * gc['frac']:.1f} % ({gr['bound']}) | {clk} MHz | "
                         f"(step, above) | | A12 (tests) |")
         ft = d.get("fit")
         if ft:
