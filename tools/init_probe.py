@@ -33,7 +33,10 @@ def main():
     ap.add_argument("--K", type=int, default=0)
     ap.add_argument("--min-sep", type=int, default=50)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--lib", default=None, help="alternative libsrt3d build (A/B)")
     args = ap.parse_args()
+    if args.lib:
+        p._lib = p.load_library(args.lib)
     f = inputs.make_frame(args.config)
     N = args.N or 16 * f.m
     K = args.K or f.K
