@@ -30,27 +30,53 @@
 
 namespace srt3d {
 
-// One warp per pixel: counts are read before the (possibly aliased) count
+// One warp per pixel, four pixels per warp iteration with every load issued
+// before any arithmetic (the counts, then the 2 x 4 rows: for m = 32 eight 8-byte
+// loads in flight per lane); counts are read before the (possibly aliased) count
 // output is written; the row's m complex values are spread over the lanes.
 // nb == nullptr: n_b[i] = offs_b[i+1] - offs_b[i] (the batch's CSR offsets).
+constexpr int MERGE_U = 4;
 __global__ void __launch_bounds__(256) merge_kernel(const float2* __restrict__ za, const uint32_t* na,
                                                     const float2* __restrict__ zb, const uint32_t* nb,
                                                     const uint32_t* offs_b, long long npix, uint32_t m, float2* zo,
                                                     uint32_t* no) {
   const int lane = threadIdx.x & 31;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < npix; i += nw) {
-    const uint32_t a = na[i];
-    const uint32_t b = nb ? nb[i] : offs_b[i + 1] - offs_b[i];
-    const uint64_t n = (uint64_t)a + b;
-    const double inv = n ? 1.0 / (double)n : 0.0;
-    const float wa = (float)((double)a * inv), wb = (float)((double)b * inv);
-    for (uint32_t j = lane; j < m; j += 32) {
-      const float2 x = za[(size_t)i * m + j], y = zb[(size_t)i * m + j];
-      zo[(size_t)i * m + j] = make_float2(fmaf(wa, x.x, wb * y.x), fmaf(wa, x.y, wb * y.y));
+  for (long long i0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * MERGE_U; i0 < npix;
+       i0 += nw * MERGE_U) {
+    uint32_t ca[MERGE_U], cb[MERGE_U];
+#pragma unroll
+    for (int u = 0; u < MERGE_U; u++) {
+      const long long i = i0 + u;
+      ca[u] = i < npix ? na[i] : 0u;
+      cb[u] = i < npix ? (nb ? nb[i] : offs_b[i + 1] - offs_b[i]) : 0u;
+    }
+    for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      float2 x[MERGE_U], y[MERGE_U];
+#pragma unroll
+      for (int u = 0; u < MERGE_U; u++) {
+        const long long i = i0 + u;
+        const bool ok = i < npix && j < m;
+        x[u] = ok ? za[(size_t)i * m + j] : make_float2(0.f, 0.f);
+        y[u] = ok ? zb[(size_t)i * m + j] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < MERGE_U; u++) {
+        const long long i = i0 + u;
+        if (i >= npix || j >= m) continue;
+        const uint64_t n = (uint64_t)ca[u] + cb[u];
+        const double inv = n ? 1.0 / (double)n : 0.0;
+        const float wa = (float)((double)ca[u] * inv), wb = (float)((double)cb[u] * inv);
+        zo[(size_t)i * m + j] = make_float2(fmaf(wa, x[u].x, wb * y[u].x), fmaf(wa, x[u].y, wb * y[u].y));
+      }
     }
     __syncwarp();
-    if (lane == 0) no[i] = (uint32_t)n;
+    uint32_t nsum = 0u;
+#pragma unroll
+    for (int u = 0; u < MERGE_U; u++)
+      if (lane == u) nsum = ca[u] + cb[u];
+    if (lane < MERGE_U && i0 + lane < npix) no[i0 + lane] = nsum;
   }
 }
 
@@ -58,8 +84,8 @@ cudaError_t launch_merge(const float* za, const uint32_t* na, const float* zb, c
                          const uint32_t* offs_b, long long npix, uint32_t m, float* zo, uint32_t* no, cudaStream_t s,
                          int num_sms) {
   if (npix <= 0) return cudaSuccess;
-  long long grid = (npix + 7) / 8;
-  if (grid > (long long)num_sms * 16) grid = (long long)num_sms * 16;
+  long long grid = (npix + 8 * MERGE_U - 1) / (8 * MERGE_U);
+  if (grid > (long long)num_sms * 8) grid = (long long)num_sms * 8;
   merge_kernel<<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const float2*>(za), na,
                                               reinterpret_cast<const float2*>(zb), nb, offs_b, npix, m,
                                               reinterpret_cast<float2*>(zo), no);
