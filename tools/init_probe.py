@@ -47,6 +47,7 @@ def main():
            "cuda_cores_forced": os.environ.get("SRT3D_INIT_CUDA_CORES", "0") == "1"}
     out["backproject_ms"] = timed(lambda: p.srt3d_backproject(z, f.sigma, f.T, N, g=g), args.reps)
     out["init_depths_ms"] = timed(lambda: p.srt3d_init_depths(z, f.sigma, f.T, N, K, args.min_sep), args.reps)
+    out["init_k1_ms"] = timed(lambda: p.srt3d_init_k1(z, f.sigma, f.T), max(args.reps, 20))
     t, ga, a, c = p.srt3d_init_depths(z, f.sigma, f.T, N, K, args.min_sep)
     torch.cuda.synchronize()
     out["mean_count"] = float(c.float().mean())
