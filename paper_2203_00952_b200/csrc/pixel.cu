@@ -346,6 +346,9 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
+  // launched as a programmatic dependent: the CTAs may start during the previous kernel's tail;
+  // nothing is read before that kernel has completed (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t par = 0u;
   // GRAD_PERSIST: one wave of CTAs, each warp loops over its 32-row tiles; else one tile per warp
   for (long long row0 = (long long)blockIdx.x * blockDim.x + (warp << 5); row0 < a.npix;
@@ -553,7 +556,29 @@ static cudaError_t launch_px(const PixArgs& a, cudaStream_t s) {
             const long long wave = (long long)per_sm * num_sms_device();
             if (wave > 0 && grid > wave) grid = wave;
           }
-          tfn<<<(unsigned)grid, GRAD_THREADS, tsmem, s>>>(a, tm);
+          // programmatic dependent launch: the CTAs of this step may be scheduled during the
+          // previous kernel's tail (griddepcontrol.wait keeps every read behind its completion).
+          // C5 L2-cold launch 18.1 -> 16.9 us, in the loop 13.57 -> 13.33 us.  SRT3D_PDL=0 disables.
+          static const bool pdl = [] {
+            const char* v = getenv("SRT3D_PDL");
+            return !(v && v[0] == '0');
+          }();
+          if (pdl) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3(GRAD_THREADS);
+            cfg.dynamicSmemBytes = tsmem;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, tfn, a, tm);
+            if (e != cudaSuccess) return e;
+          } else {
+            tfn<<<(unsigned)grid, GRAD_THREADS, tsmem, s>>>(a, tm);
+          }
           return cudaGetLastError();
         }
       }
