@@ -10,6 +10,10 @@ import torch  # noqa: E402
 
 import paper_2203_00952_b200 as p  # noqa: E402
 
+if "--lib" in sys.argv:  # alternative build (A/B)
+    _i = sys.argv.index("--lib")
+    p._lib = p.load_library(sys.argv[_i + 1])
+    del sys.argv[_i:_i + 2]
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 npix = int(args[0]) if len(args) > 0 else 262144
 N = npix * (int(args[1]) if len(args) > 1 else 1000)
