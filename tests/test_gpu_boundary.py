@@ -185,3 +185,47 @@ def test_reentrant_two_threads_two_streams(gpu, inputs_mod):
         for it_ref, it_res in zip(ref[k], res[k]):
             for u, v in zip(it_ref, it_res):
                 assert torch.equal(u.view(torch.uint8), v.view(torch.uint8))
+
+
+_PDL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2203_00952_b200 as p
+from paper_2203_00952_b200.pipeline import FramePipeline  # noqa: F401  (same package state as the bench)
+g = torch.Generator(device="cuda").manual_seed(3)
+npix, m, K, T, sigma = 70001, 32, 3, 8192, 6.0
+t = torch.rand((npix, K), device="cuda", generator=g) * T
+a = torch.rand((npix, K), device="cuda", generator=g)
+z = torch.randn((npix, m), dtype=torch.complex64, device="cuda", generator=g)
+s = torch.cuda.Stream()
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph, stream=s):
+    for _ in range(7):
+        p.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5, stream=s)
+graph.replay()
+for _ in range(3):  # and as ordinary stream launches behind other kernels
+    z.mul_(1.0)
+    p.srt3d_sketch_grad_step(z, t, a, sigma, T, m, 0.5)
+torch.cuda.synchronize()
+np.save(sys.argv[2], np.concatenate([t.cpu().numpy().ravel(), a.cpu().numpy().ravel()]))
+"""
+
+
+def test_programmatic_dependent_launch_bitwise(tmp_path):
+    """The TMA gradient step is launched as a programmatic dependent (griddepcontrol.wait before
+    any global read): graph-replayed and stream-ordered steps give bitwise the
+    theta of ordinary launches (SRT3D_PDL=0)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = tmp_path / f"theta_{flag}.npy"
+        env = dict(os.environ, SRT3D_PDL=flag)
+        r = subprocess.run([sys.executable, "-c", _PDL_SCRIPT, root, str(out)], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
