@@ -204,7 +204,12 @@ int srt3d_descent_update(float* t, float* alpha, const float* grad_t, const floa
  * srt3d_sketch_grad_step — srt3d_sketch_grad followed by
  * srt3d_descent_update in ONE kernel (same arithmetic, grad_t / grad_alpha
  * never leave registers).  loss may be NULL.  t and alpha are updated in
- * place; each pixel's reads of t/alpha precede its writes.
+ * place; each pixel's reads of t/alpha precede its writes.  For m % 16 == 0
+ * (TMA z staging) the kernel is launched as a programmatic dependent of the
+ * previous work on the stream: its CTAs may be scheduled during that work's
+ * tail but read nothing before it has completed (griddepcontrol.wait), so
+ * stream order is unchanged; the environment variable SRT3D_PDL=0 (read once
+ * per process) launches it as an ordinary kernel.
  */
 int srt3d_sketch_grad_step(const float* z, float* t, float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,
                            uint32_t m, float eta, float* loss, void* stream);
