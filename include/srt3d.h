@@ -142,6 +142,7 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
 #define SRT3D_PATH_BINCOUNT 2
 #define SRT3D_PATH_PAIRED 3
 #define SRT3D_PATH_ROUTED 4
+#define SRT3D_PATH_TENSOR 5
 #define SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN 1.0
 #define SRT3D_HINT_UNKNOWN 0ull
 int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix, uint32_t T, uint32_t m, float* z,

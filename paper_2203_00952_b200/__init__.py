@@ -32,7 +32,7 @@ _lib = None
 
 SRT3D_OK = 0
 ERRORS = {-1: "SRT3D_EINVAL", -2: "SRT3D_ENULL", -3: "SRT3D_EUNSUPPORTED", -4: "SRT3D_ECUDA", -5: "SRT3D_EALIGN"}
-PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT, PATH_PAIRED, PATH_ROUTED = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_DIRECT, PATH_BINCOUNT, PATH_PAIRED, PATH_ROUTED, PATH_TENSOR = 0, 1, 2, 3, 4, 5
 HINT_UNKNOWN = 0
 EXPORTS = ("srt3d_version", "srt3d_last_error", "srt3d_sketch", "srt3d_sketch_ex", "srt3d_expected_sketch",
            "srt3d_sketch_grad",

@@ -144,9 +144,11 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
   if (npix < 0) return fail(SRT3D_EINVAL, "npix=%lld < 0", (long long)npix);
   int rc = check_tm(T, m);
   if (rc) return rc;
-  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_ROUTED) return fail(SRT3D_EINVAL, "path=%d unknown", path);
+  if (path < SRT3D_PATH_AUTO || path > SRT3D_PATH_TENSOR) return fail(SRT3D_EINVAL, "path=%d unknown", path);
   if (path == SRT3D_PATH_ROUTED && lanes_per_pixel != 0 && lanes_per_pixel != 2)
     return fail(SRT3D_EINVAL, "routed path: lanes_per_pixel=%d must be 0 or 2", lanes_per_pixel);
+  if (path == SRT3D_PATH_TENSOR && lanes_per_pixel != 0)
+    return fail(SRT3D_EINVAL, "tensor-core path: lanes_per_pixel=%d must be 0", lanes_per_pixel);
   if (path != SRT3D_PATH_ROUTED && lanes_per_pixel != 0 && lanes_per_pixel != 4 && lanes_per_pixel != 8 &&
       lanes_per_pixel != 16 && lanes_per_pixel != 32)
     return fail(SRT3D_EINVAL, "lanes_per_pixel=%d must be 0, 4, 8, 16 or 32", lanes_per_pixel);
@@ -161,6 +163,8 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
     return fail(SRT3D_EUNSUPPORTED, "class-sorted path needs T <= %u (T=%u)", srt3d::SO_MAX_T, T);
   if (path == SRT3D_PATH_ROUTED && !srt3d::routed_fits(T, 0))
     return fail(SRT3D_EUNSUPPORTED, "routed path needs T %% 4 == 0 and T <= %u (T=%u)", srt3d::RT_MAX_T, T);
+  if (path == SRT3D_PATH_TENSOR && !srt3d::tc_fits(T))
+    return fail(SRT3D_EUNSUPPORTED, "tensor-core path needs T <= %u (T=%u)", srt3d::TC_MAX_T, T);
   cudaStream_t s = (cudaStream_t)stream;
   const int nsm = num_sms_current();
   srt3d::SketchArgs a = {};
@@ -177,6 +181,8 @@ int sketch_entry(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
     cudaError_t e = cudaSuccess;
     if (path == SRT3D_PATH_PAIRED) {
       e = srt3d::launch_sketch_pair(M, a, s, nsm);
+    } else if (path == SRT3D_PATH_TENSOR) {
+      e = srt3d::launch_sketch_tc(M, a, s, nsm);
     } else if (path == SRT3D_PATH_ROUTED) {
       e = j0 == 0 ? srt3d::launch_sketch_routed(M, a, s, nsm)
                   : srt3d::launch_sketch_pass(M, M >= 24 ? srt3d::SK_G4_CHEB : 4, a, s, nsm);

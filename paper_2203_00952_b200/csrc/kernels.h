@@ -54,6 +54,9 @@ enum : uint32_t { RG_NONE = 0, RG_G4, RG_G8, RG_G16, RG_G32, RG_G4C, RG_RT, RG_H
 // class-routed Chebyshev kernel (sketch_routed.cu): first pass only, T % 4 == 0, T <= RT_MAX_T
 constexpr uint32_t RT_MAX_T = 12000;  // 1.25 T phasor entries + T class bytes + [32][512] fp32 partials + spills <= 227 KB
 __host__ __device__ inline bool routed_fits(uint32_t T, uint32_t j0) { return j0 == 0 && T % 4 == 0 && T <= RT_MAX_T; }
+// tensor-core sketch (sketch_tc.cu): Kb = 64 ceil(T / 2048) <= 256 columns per row, R = ceil(T / Kb) <= 32 rows
+constexpr uint32_t TC_MAX_T = 8192;
+__host__ __device__ inline bool tc_fits(uint32_t T) { return T >= 1 && T <= TC_MAX_T; }
 enum : uint32_t { RGM_AUTO = 0, RGM_DIRECT = 1, RGM_HIST = 2 };
 constexpr uint32_t SK_TABLE_MAX_T = 24575;  // (T + 1) float2 entries fit SK_MAX_SMEM
 // mode: RGM_AUTO (bin-count allowed: the host passes it only when the
@@ -183,6 +186,9 @@ cudaError_t launch_sketch_pair(int M, const SketchArgs& a, cudaStream_t s, int n
 cudaError_t launch_sketch_routed(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
 size_t sketch_routed_smem(uint32_t T, int M);
 size_t sketch_pair_smem(uint32_t T);
+// tensor-core sketch (sketch_tc.cu): T <= TC_MAX_T, one pass of M <= 32 frequencies
+cudaError_t launch_sketch_tc(int M, const SketchArgs& a, cudaStream_t s, int num_sms);
+size_t sketch_tc_smem(uint32_t T, int MP);
 cudaError_t launch_phase_index(const uint16_t* bins, long long n, uint32_t T, uint32_t m, uint32_t* r,
                                cudaStream_t s, int num_sms);
 cudaError_t launch_check_csr(const uint16_t* bins, const uint32_t* offsets, long long npix, uint32_t T,

@@ -1,0 +1,412 @@
+// K6 — tensor-core sketch, Eq. (3) regrouped
+// by bin and factored once (a radix-Kb Cooley–Tukey step):
+//
+//   z_ij = (1/n_i) sum_p e^{i w_j x_p}                           (Eq. 3, w_j = 2 pi j / T)
+//        = (1/n_i) sum_x h_i[x] e^{i w_j x}                        (h_i: photon counts per bin)
+//   x = Kb a + b  (0 <= b < Kb, 0 <= a < R = ceil(T / Kb) <= 32):
+//        = (1/n_i) sum_a e^{i w_j Kb a} [ sum_b h_i[a][b] e^{i w_j b} ]
+//        = (1/n_i) sum_a W[a][j] P_i[a][j],   P_i = H_i V   (H_i: R x Kb, V: Kb x m)
+//
+// P = H V is a dense contraction over b with one V for every pixel and row:
+// it runs on the 5th-generation tensor cores (tcgen05.mma kind::f16, M = 128
+// rows = 4 pixels x 32 rows a, N = 4 MP columns, K = Kb), the twiddle by W and
+// the sum over a on the CUDA cores in the epilogue (a warp per pixel: lane = a).
+//
+// Exactness of the operands:
+//  * H: integer counts c < 2048 held as the raw bits of an fp16 number.  The
+//    fp16 subnormal / first-normal binade is linear in its bit pattern:
+//    bits c encode exactly c * 2^-24 for 0 <= c < 2048, so the shared-memory
+//    histogram is built with plain integer atomics on packed u16 pairs and fed
+//    to the MMA as is (no conversion pass); the epilogue multiplies by 2^24.
+//    A pixel with more than CNT_MAX photons is split into rounds of at most
+//    CNT_MAX photons whose MMAs accumulate into the same TMEM columns, so no
+//    count ever reaches 2048.
+//  * V = cos / sin (w_j b) from the exact phase index (j b) mod T in fp64,
+//    split V = hi + 2^-12 lo with hi = fp16(V), lo = fp16(2^12 (V - hi)):
+//    |V - hi - 2^-12 lo| <= 2^-24 (6e-8).  B = [cos hi | sin hi | cos lo |
+//    sin lo] (N = 4 MP columns); products are exact in the fp32 accumulator.
+//  * W[a][j] = e^{i w_j Kb a} from the exact phase index (j Kb a) mod T in
+//    fp64, rounded to fp32.
+//
+// Roles (one persistent CTA per SM, 13 warps):
+//  * warps 4..11 (builders): per unit (a tile of 4 pixels, or one round of a
+//    heavy tile) zero an A stage, scatter the photons into it with shared-
+//    memory atomics (16-byte vector loads of the tile's contiguous CSR range,
+//    issued one tile ahead), fence to the async proxy, arrive on full[s];
+//  * warp 12, one thread (MMA issuer): waits full[s] (and the TMEM buffer's
+//    accempty), issues 4 KA tcgen05.mma, commits to empty[s] (A stage free)
+//    and, after a tile's last round, to accfull[tb];
+//  * warps 0..3 (epilogue): warp w = pixel w of the tile = TMEM lanes 32w..;
+//    reads its N accumulator columns, combines hi + lo, twiddles by W[lane],
+//    reduce-scatters the 2 MP values across the warp (lane l ends with
+//    frequency l), scales by 2^24 / n and stores z coalesced.
+// Two A stages and two TMEM accumulators: the scatter of tile t + 1, the MMAs
+// of tile t and the epilogue of tile t - 1 run concurrently.
+// Supported: T <= TC_MAX_T (Kb <= 256, R <= 32), one pass of M <= 32
+// frequencies (MP = 16 for M <= 16, else 32).
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace srt3d {
+
+namespace {
+
+constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_BLD_WARPS = 8;                 // two per pixel slot of a tile
+constexpr int TC_SLOT_THREADS = 64;
+constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_BLD_WARPS;
+constexpr int TC_THREADS_ALL = (TC_MMA_WARP + 1) * 32;
+constexpr uint32_t CNT_MAX = 2040;      // photons of one pixel per round: every count < 2048, <= 256 groups
+constexpr int PF = 4;                   // 16-byte photon groups per builder thread (64 x 4 x 8 >= CNT_MAX + 7)
+// per-unit flags (builders -> MMA issuer, through shared memory under the full barrier)
+constexpr uint32_t UF_FIRST = 1, UF_LAST = 2, UF_END = 4, UF_TB = 8;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// canonical K-major SWIZZLE_NONE operand: 8 x 16-byte core matrices (128 B each),
+// LBO = 128 B between K-adjacent core matrices, SBO between 8-row groups
+__device__ __forceinline__ uint64_t ns_desc(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TCS_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra TCS_WAIT_%=;\n\t}" ::"r"(su32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
+}
+
+// Kb = K columns per row (power of two, 16..256) and its log2: 32 rows x Kb >= T
+__host__ __device__ inline uint32_t tc_log2_kb(uint32_t T) {
+  uint32_t q = 4;
+  while ((32u << q) < T) q++;
+  return q;
+}
+
+// The bin x of a photon IS its element index in its pixel's 32 x Kb block:
+// with x's bits read as [a_hi (2) | k_hi (q - 3) | a_lo (3) | k_lo (3)] the
+// block's K-major SWIZZLE_NONE layout [a_hi][k_hi][a_lo][k_lo] (row a = 8 a_hi
+// + a_lo, column k = 8 k_hi + k_lo) puts bin x at fp16 element x, and
+//   x = X_row(a) + X_col(k),  X_row(a) = 8 Kb a_hi + 8 a_lo,  X_col(k) = 64 k_hi + k_lo,
+// so e^{i w x} = W[a] V[k] with W[a] = e^{i w X_row(a)}, V[k] = e^{i w X_col(k)}.
+__host__ __device__ inline uint32_t tc_xrow(uint32_t a, uint32_t q) { return ((a >> 3) << (q + 3)) + ((a & 7u) << 3); }
+__host__ __device__ inline uint32_t tc_xcol(uint32_t k) { return ((k >> 3) << 6) + (k & 7u); }
+
+template <int MP>
+__global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs a, uint32_t M) {
+  extern __shared__ unsigned char tcs_raw[];
+  if (sketch_regime_skip(a, (int)M)) return;  // another candidate launch of this pass does the work
+  constexpr int N = 4 * MP;
+  unsigned char* sm = tcs_raw + ((128u - (su32(tcs_raw) & 127u)) & 127u);
+  const uint32_t T = a.T;
+  const uint32_t q = tc_log2_kb(T), Kb = 1u << q;
+  const uint32_t SLOT_B = 64u * Kb;          // bytes of one pixel's 32 x Kb fp16 block
+  const uint32_t ASZ = 4u * SLOT_B;          // one A stage: 128 rows
+  const uint32_t SBO = 16u * Kb;             // bytes between 8-row groups (A and B)
+  unsigned char* A0 = sm;
+  unsigned char* Bs = sm + 2 * ASZ;
+  float2* Ws = reinterpret_cast<float2*>(Bs + (size_t)N * Kb * 2u);  // [MP][32] (frequency-major)
+  __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], accfull_bar[2], accempty_bar[2];
+  __shared__ uint32_t tmem_slot, uflags[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- one-time setup: B (hi | lo split), W, zeroed A stages, barriers, TMEM ----
+  for (uint32_t e = tid; e < (uint32_t)MP * Kb; e += TC_THREADS_ALL) {
+    const uint32_t jj = e >> q, k = e & (Kb - 1u);
+    __half h[4] = {__float2half(0.f), __float2half(0.f), __float2half(0.f), __float2half(0.f)};
+    if (jj < M) {
+      const uint32_t j = a.j0 + 1u + jj;
+      const uint32_t r = (uint32_t)(((unsigned long long)j * tc_xcol(k)) % T);
+      double sn, c;
+      sincospi(2.0 * (double)r / (double)T, &sn, &c);
+      const __half ch = __double2half(c), sh = __double2half(sn);
+      h[0] = ch;
+      h[1] = sh;
+      h[2] = __double2half((c - (double)__half2float(ch)) * 4096.0);
+      h[3] = __double2half((sn - (double)__half2float(sh)) * 4096.0);
+    }
+#pragma unroll
+    for (int g = 0; g < 4; g++) {
+      const uint32_t n = (uint32_t)g * MP + jj;
+      *reinterpret_cast<__half*>(Bs + (n >> 3) * SBO + (k >> 3) * 128u + (n & 7u) * 16u + (k & 7u) * 2u) = h[g];
+    }
+  }
+  for (uint32_t e = tid; e < (uint32_t)MP * 32u; e += TC_THREADS_ALL) {
+    const uint32_t jj = e >> 5, ar = e & 31u, xr = tc_xrow(ar, q);
+    float2 w = make_float2(0.f, 0.f);
+    if (jj < M && xr < T) {
+      const uint32_t j = a.j0 + 1u + jj;
+      const uint32_t r = (uint32_t)(((unsigned long long)j * xr) % T);
+      double sn, c;
+      sincospi(2.0 * (double)r / (double)T, &sn, &c);
+      w = make_float2((float)c, (float)sn);
+    }
+    Ws[e] = w;
+  }
+  for (uint32_t e = tid; e < 2 * ASZ / 16; e += TC_THREADS_ALL)
+    reinterpret_cast<uint4*>(A0)[e] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) {
+    for (int s = 0; s < 2; s++) {
+      mbar_init(&full_bar[s], TC_BLD_WARPS);
+      mbar_init(&empty_bar[s], 1);
+      mbar_init(&accfull_bar[s], 1);
+      mbar_init(&accempty_bar[s], TC_EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(2u * N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+  const long long ntiles = (a.npix + 3) / 4;
+
+  if (warp >= TC_EPI_WARPS && warp < TC_MMA_WARP) {
+    // ======================= builders: warps 4 + 2k, 5 + 2k own pixel slot k =======================
+    const uint32_t slot = (uint32_t)(warp - TC_EPI_WARPS) >> 1;
+    const uint32_t pt = (uint32_t)tid & 63u;
+    const uint32_t esh = (uint32_t)(reinterpret_cast<uintptr_t>(a.bins) >> 1) & 7u;  // elements before 16 B alignment
+    const uint4* gb = reinterpret_cast<const uint4*>(a.bins - esh);
+    // the photon range of (pixel p, round r): [b0, b1); this thread's groups of it
+    auto range = [&](long long p, uint32_t r, uint32_t& b0, uint32_t& b1) {
+      if (p < a.npix) {
+        const uint32_t o0 = a.offsets[p], o1 = a.offsets[p + 1];
+        b0 = o0 + r * CNT_MAX;
+        b1 = min(o1, b0 + CNT_MAX);
+        if (b0 > b1) b0 = b1;
+      } else {
+        b0 = b1 = 0;
+      }
+    };
+    auto load_groups = [&](uint32_t b0, uint32_t b1, uint4 (&v)[PF]) {
+      const uint32_t G0 = (b0 + esh) >> 3, G1 = (b1 + esh + 7u) >> 3;
+#pragma unroll
+      for (int g = 0; g < PF; g++) {
+        const uint32_t G = G0 + pt + (uint32_t)g * TC_SLOT_THREADS;
+        v[g] = (b0 < b1 && G < G1) ? __ldg(gb + G) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    // rounds of a tile: the largest pixel count of its 4 pixels, in CNT_MAX units
+    auto tile_rounds = [&](long long t) -> uint32_t {
+      uint32_t mx = 0;
+      for (int k = 0; k < 4; k++) {
+        const long long p = 4 * t + k;
+        if (p < a.npix) mx = max(mx, a.offsets[p + 1] - a.offsets[p]);
+      }
+      return mx == 0 ? 1u : (mx + CNT_MAX - 1) / CNT_MAX;
+    };
+    long long t = blockIdx.x;
+    uint32_t b0 = 0, b1 = 0, nb0 = 0, nb1 = 0;
+    uint4 cur[PF], nxt[PF];
+    range(4 * t + slot, 0, b0, b1);
+    load_groups(b0, b1, cur);
+    uint32_t rounds = tile_rounds(t);
+    uint32_t unit = 0, lt = 0;
+    for (; t < ntiles; t += gridDim.x, lt++) {
+      const long long tn = t + gridDim.x;
+      const uint32_t rounds_n = tn < ntiles ? tile_rounds(tn) : 1u;
+      for (uint32_t r = 0; r < rounds; r++, unit++) {
+        const uint32_t s = unit & 1u;
+        unsigned char* Ab = A0 + s * ASZ + slot * SLOT_B;
+        if (r > 0) {  // heavy pixel rounds: this round's groups now
+          range(4 * t + slot, r, b0, b1);
+          load_groups(b0, b1, cur);
+        }
+        if (r + 1 == rounds && tn < ntiles) {  // next tile's first round, one tile ahead
+          range(4 * tn + slot, 0, nb0, nb1);
+          load_groups(nb0, nb1, nxt);
+        }
+        if (unit >= 2) {
+          mbar_wait(&empty_bar[s], ((unit >> 1) - 1u) & 1u);  // MMAs of unit - 2 done with this stage
+          for (uint32_t e = pt; e < SLOT_B / 16; e += TC_SLOT_THREADS)
+            reinterpret_cast<uint4*>(Ab)[e] = make_uint4(0u, 0u, 0u, 0u);
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(TC_SLOT_THREADS) : "memory");
+        }
+        if (b0 < b1) {
+          const uint32_t G0 = (b0 + esh) >> 3;
+          const uint32_t lo = b0 + esh, hi = b1 + esh;  // element indices relative to the aligned base
+#pragma unroll
+          for (int g = 0; g < PF; g++) {
+            const uint32_t G = G0 + pt + (uint32_t)g * TC_SLOT_THREADS;
+            const uint32_t w4[4] = {cur[g].x, cur[g].y, cur[g].z, cur[g].w};
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+              const uint32_t gi = 8u * G + (uint32_t)e;
+              const uint32_t x = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+              // x < T: an out-of-range bin (precondition violation) is the zero "absent photon" term
+              if (gi >= lo && gi < hi && x < T)
+                atomicAdd(reinterpret_cast<uint32_t*>(Ab + ((x << 1) & ~3u)), 1u << ((x & 1u) << 4));
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (tid == TC_EPI_WARPS * 32)
+          uflags[s] = (r == 0 ? UF_FIRST : 0u) | (r + 1 == rounds ? UF_LAST : 0u) |
+                      (r + 1 == rounds && tn >= ntiles ? UF_END : 0u) | ((lt & 1u) ? UF_TB : 0u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_bar[s]);
+      }
+      rounds = rounds_n;
+      b0 = nb0;
+      b1 = nb1;
+#pragma unroll
+      for (int g = 0; g < PF; g++) cur[g] = nxt[g];
+    }
+  } else if (warp == TC_MMA_WARP) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      // D f32, A/B f16, both K-major, N, M = 128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint32_t sa0 = su32(A0), sb = su32(Bs);
+      uint32_t lt = 0;
+      for (uint32_t unit = 0;; unit++) {
+        const uint32_t s = unit & 1u;
+        mbar_wait(&full_bar[s], (unit >> 1) & 1u);
+        const uint32_t f = uflags[s];
+        const uint32_t tb = (f & UF_TB) ? 1u : 0u;
+        if ((f & UF_FIRST) && lt >= 2) mbar_wait(&accempty_bar[tb], ((lt >> 1) - 1u) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = sa0 + s * ASZ;
+        for (uint32_t kk = 0; kk < Kb / 16; kk++)  // K step of 16 = two core matrices along K
+          mma_f16(tmem + tb * (uint32_t)N, ns_desc(sa + kk * 256u, SBO), ns_desc(sb + kk * 256u, SBO), idesc,
+                  (!(f & UF_FIRST) || kk > 0) ? 1u : 0u);
+        commit(&empty_bar[s]);
+        if (f & UF_LAST) {
+          commit(&accfull_bar[tb]);
+          lt++;
+        }
+        if (f & UF_END) break;
+      }
+    }
+  } else {
+    // ======================= epilogue =======================
+    constexpr int NV = 2 * MP;
+    uint32_t lt = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+      const uint32_t tb = lt & 1u;
+      const long long p = 4 * t + warp;
+      uint32_t n = 0;
+      if (p < a.npix) n = a.offsets[p + 1] - a.offsets[p];
+      mbar_wait(&accfull_bar[tb], (lt >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + tb * (uint32_t)N + ((uint32_t)(warp * 32) << 16);
+      float acc[NV];
+#pragma unroll
+      for (int g = 0; g < MP / 8; g++) {
+        float ch[8], sh[8], cl[8], sl[8];
+        tmem_ld8(base + 0 * MP + 8 * g, ch);
+        tmem_ld8(base + 1 * MP + 8 * g, sh);
+        tmem_ld8(base + 2 * MP + 8 * g, cl);
+        tmem_ld8(base + 3 * MP + 8 * g, sl);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const int jj = 8 * g + k;
+          const float pc = fmaf(cl[k], 0.000244140625f, ch[k]);  // hi + 2^-12 lo
+          const float ps = fmaf(sl[k], 0.000244140625f, sh[k]);
+          const float2 w = Ws[jj * 32 + lane];
+          acc[2 * jj] = fmaf(w.x, pc, -w.y * ps);
+          acc[2 * jj + 1] = fmaf(w.x, ps, w.y * pc);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty_bar[tb]);
+      // reduce-scatter over the 32 rows a (lanes): lane l keeps value indices with its bits
+#pragma unroll
+      for (int o = 16, h = NV / 2; o >= 1; o >>= 1, h >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; i++) {
+          const float send = up ? acc[i] : acc[i + h];
+          const float keep = up ? acc[i + h] : acc[i];
+          acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (p < a.npix) {
+        const float sc = n ? (float)(16777216.0 / (double)n) : 0.f;  // 2^24 (count encoding) / n
+        float2* zp = reinterpret_cast<float2*>(a.z) + (size_t)p * a.mstride + a.j0;
+        if constexpr (MP == 32) {
+          if ((uint32_t)lane < M) zp[lane] = make_float2(acc[0] * sc, acc[1] * sc);
+        } else {
+          if ((uint32_t)(lane >> 1) < M) reinterpret_cast<float*>(zp)[lane] = acc[0] * sc;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N));
+}
+
+template <int MP>
+cudaError_t launch_tc_t(const SketchArgs& a, uint32_t M, cudaStream_t s, int num_sms) {
+  auto fn = sketch_tc_kernel<MP>;
+  static SmemAttrOnce attr;
+  cudaError_t e = smem_attr_once(attr, fn, (int)sketch_tc_smem(TC_MAX_T, MP));
+  if (e != cudaSuccess) return e;
+  const long long tiles = (a.npix + 3) / 4;
+  long long grid = num_sms;  // one persistent CTA per SM (shared memory, TMEM)
+  if (grid > tiles) grid = tiles;
+  if (grid < 1) grid = 1;
+  fn<<<(unsigned)grid, TC_THREADS_ALL, sketch_tc_smem(a.T, MP), s>>>(a, M);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t sketch_tc_smem(uint32_t T, int MP) {
+  const size_t Kb = (size_t)1 << tc_log2_kb(T);
+  return 128 + 2 * 256 * Kb + (size_t)4 * MP * Kb * 2 + (size_t)MP * 32 * sizeof(float2);
+}
+
+cudaError_t launch_sketch_tc(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
+  if (!tc_fits(a.T) || M < 1 || M > 32) return cudaErrorInvalidValue;
+  if (M <= 16) return launch_tc_t<16>(a, (uint32_t)M, s, num_sms);
+  return launch_tc_t<32>(a, (uint32_t)M, s, num_sms);
+}
+
+}  // namespace srt3d

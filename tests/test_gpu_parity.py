@@ -150,7 +150,14 @@ def test_sketch_lane_regimes_forced(gpu, oracle_mod, inputs_mod):
 def _routed_ok(T):
     return T % 4 == 0 and T <= 12000
 
-CLASS_PATHS = [("paired", 3, 0), ("routed", 4, 0)]
+
+def _path_ok(path, T):
+    """False where the forced path must refuse T with SRT3D_EUNSUPPORTED (routed: T % 4 == 0 and
+    T <= 12000; tensor-core: T <= 8192)."""
+    return (path != 4 or _routed_ok(T)) and (path != 5 or T <= 8192)
+
+
+CLASS_PATHS = [("paired", 3, 0), ("routed", 4, 0), ("tensor", 5, 0)]
 
 
 @pytest.mark.parametrize("which,path,lanes", CLASS_PATHS)
@@ -166,7 +173,7 @@ def test_sketch_class_paths_parity(gpu, oracle_mod, inputs_mod, which, path, lan
     import torch
 
     bins, offs = inputs_mod.random_csr(npix=333, T=T, max_n=max_n, seed=T * 3 + m + max_n)
-    if path == 4 and not _routed_ok(T):  # the routed path needs T % 4 == 0, T <= 12000: it must say so
+    if not _path_ok(path, T):  # routed: T % 4 == 0, T <= 12000; tensor: T <= 8192 — it must say so
         with pytest.raises(gpu.Srt3dError) as e:
             gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, m, path=path)
         assert e.value.code == -3
@@ -195,7 +202,7 @@ def test_sketch_class_paths_worst_bins(gpu, oracle_mod, which, path, lanes, T):
     lists.append(list(np.arange(2000) % 7))          # class A/B mix at tiny bins
     lists.append([T // 4] * 1500 + [0] * 5)           # almost one class, then the other
     bins, offs = _csr(lists)
-    if path == 4 and not _routed_ok(T):
+    if not _path_ok(path, T):
         return
     for m in (32, 64):
         z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, min(m, T - 1), total_photons=int(offs[-1]),
@@ -224,7 +231,7 @@ def test_sketch_class_paths_alignment_and_determinism(gpu, oracle_mod, inputs_mo
     z2 = _host(gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=path, lanes_per_pixel=lanes))
     assert np.array_equal(z1.view(np.uint64), z2.view(np.uint64))
     with pytest.raises(gpu.Srt3dError):
-        gpu.srt3d_sketch_ex(db, do, 12004 if path == 4 else 23801, m, path=path, lanes_per_pixel=lanes)
+        gpu.srt3d_sketch_ex(db, do, {4: 12004, 5: 8193}.get(path, 23801), m, path=path, lanes_per_pixel=lanes)
 
 
 def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):

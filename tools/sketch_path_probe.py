@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--m", type=int, default=None)
+    ap.add_argument("--only", default=None, help="comma-separated variant names (auto always runs)")
     ap.add_argument("--lib", default=None, help="alternative libsrt3d build (tuning variants)")
     args = ap.parse_args()
     if args.lib:
@@ -29,7 +30,9 @@ def main():
     bins, offs = torch.from_numpy(f.bins).cuda(), torch.from_numpy(f.offsets).cuda()
     out = {"config": args.config, "n": args.n, "m": m, "T": f.T, "photons": f.n_photons}
     variants = [("auto", p.PATH_AUTO, 0), ("sorted", p.PATH_PAIRED, 0), ("g4", p.PATH_DIRECT, 4),
-                ("g8", p.PATH_DIRECT, 8), ("routed", p.PATH_ROUTED, 0)]
+                ("g8", p.PATH_DIRECT, 8), ("routed", p.PATH_ROUTED, 0), ("tensor", p.PATH_TENSOR, 0)]
+    if args.only:
+        variants = [v for v in variants if v[0] in args.only.split(",") or v[0] == "auto"]
     zs = {}
     for name, path, lanes in variants:
         z = torch.empty((f.npix, m), dtype=torch.complex64, device="cuda")
