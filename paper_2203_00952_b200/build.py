@@ -12,12 +12,14 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libsrt3d.so")
+# A/B variants (tools only): SRT3D_VARIANT=tag SRT3D_EXTRA="-DX=1" builds tools/libsrt3d_<tag>.so
+_VARIANT = os.environ.get("SRT3D_VARIANT")
+OBJ = os.path.join(HERE, "build" + ("_" + _VARIANT if _VARIANT else ""))
+LIB = (os.path.join(HERE, "..", "tools", f"libsrt3d_{_VARIANT}.so") if _VARIANT else os.path.join(HERE, "libsrt3d.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-                "-I", os.path.join(HERE, "..", "include")]
+                "-I", os.path.join(HERE, "..", "include")] + os.environ.get("SRT3D_EXTRA", "").split()
 
 
 def _sources():

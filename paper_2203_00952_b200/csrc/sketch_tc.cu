@@ -55,7 +55,7 @@ namespace srt3d {
 
 namespace {
 
-constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_EPI_WARPS = 8;                 // two per pixel slot: warp w reads TMEM lanes 32 (w % 4), frequency half w / 4
 constexpr int TC_BLD_WARPS = 8;                 // two per pixel slot of a tile
 constexpr int TC_SLOT_THREADS = 64;
 constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_BLD_WARPS;
@@ -63,6 +63,7 @@ constexpr int TC_THREADS_ALL = (TC_MMA_WARP + 1) * 32;
 constexpr uint32_t CNT_MAX = 2040;      // photons of one pixel per round: every count < 2048, <= 256 groups
 constexpr int PF = 4;                   // 16-byte photon groups per builder thread (64 x 4 x 8 >= CNT_MAX + 7)
 // per-unit flags (builders -> MMA issuer, through shared memory under the full barrier)
+constexpr uint32_t TC_TPC_MAX = 768;  // tiles per CTA per launch (offsets staged in shared memory)
 constexpr uint32_t UF_FIRST = 1, UF_LAST = 2, UF_END = 4, UF_TB = 8;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -103,7 +104,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -128,8 +129,19 @@ __host__ __device__ inline uint32_t tc_log2_kb(uint32_t T) {
 __host__ __device__ inline uint32_t tc_xrow(uint32_t a, uint32_t q) { return ((a >> 3) << (q + 3)) + ((a & 7u) << 3); }
 __host__ __device__ inline uint32_t tc_xcol(uint32_t k) { return ((k >> 3) << 6) + (k & 7u); }
 
+#ifdef TC_PROF
+// tools-only timing build (SRT3D_EXTRA=-DTC_PROF): per-role cycle counters summed over CTAs
+__device__ unsigned long long tc_prof[16];
+#define TCP_T0 const long long _tcp0 = clock64();
+#define TCP_ADD(i, t0) atomicAdd(&tc_prof[i], (unsigned long long)(clock64() - (t0)))
+#else
+#define TCP_T0
+#define TCP_ADD(i, t0)
+#endif
+
 template <int MP>
-__global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs a, uint32_t M) {
+__global__ void __launch_bounds__(TC_THREADS_ALL, 1)
+    sketch_tc_kernel(SketchArgs a, uint32_t M, long long pbase, long long pcount, uint32_t tpc) {
   extern __shared__ unsigned char tcs_raw[];
   if (sketch_regime_skip(a, (int)M)) return;  // another candidate launch of this pass does the work
   constexpr int N = 4 * MP;
@@ -142,6 +154,8 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
   unsigned char* A0 = sm;
   unsigned char* Bs = sm + 2 * ASZ;
   float2* Ws = reinterpret_cast<float2*>(Bs + (size_t)N * Kb * 2u);  // [MP][32] (frequency-major)
+  uint32_t* so = reinterpret_cast<uint32_t*>(Ws + MP * 32);            // this CTA's offsets [4 ntl + 1]
+  uint32_t* rounds_s = so + 4 * TC_TPC_MAX + 1;                         // rounds per local tile [ntl]
   __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], accfull_bar[2], accempty_bar[2];
   __shared__ uint32_t tmem_slot, uflags[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -181,6 +195,19 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
   }
   for (uint32_t e = tid; e < 2 * ASZ / 16; e += TC_THREADS_ALL)
     reinterpret_cast<uint4*>(A0)[e] = make_uint4(0u, 0u, 0u, 0u);
+  // this CTA's tiles: [t0, t0 + ntl) of the launch's ceil(pcount / 4); its pixels' offsets staged
+  // in shared memory (pixels past the launch's range repeat the last offset: empty)
+  const long long ntiles = (pcount + 3) / 4;
+  const long long t0 = (long long)blockIdx.x * tpc;
+  const uint32_t ntl = (uint32_t)max(0ll, min((long long)tpc, ntiles - t0));
+  const long long p0 = pbase + 4 * t0, pend = pbase + pcount;
+  for (uint32_t i = tid; i <= 4 * ntl; i += TC_THREADS_ALL) so[i] = a.offsets[min(p0 + (long long)i, pend)];
+  __syncthreads();
+  for (uint32_t i = tid; i < ntl; i += TC_THREADS_ALL) {
+    uint32_t mx = 0;
+    for (int k = 0; k < 4; k++) mx = max(mx, so[4 * i + k + 1] - so[4 * i + k]);
+    rounds_s[i] = mx == 0 ? 1u : (mx + CNT_MAX - 1) / CNT_MAX;
+  }
   if (tid == 0) {
     for (int s = 0; s < 2; s++) {
       mbar_init(&full_bar[s], TC_BLD_WARPS);
@@ -200,26 +227,22 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
-  const long long ntiles = (a.npix + 3) / 4;
 
   if (warp >= TC_EPI_WARPS && warp < TC_MMA_WARP) {
-    // ======================= builders: warps 4 + 2k, 5 + 2k own pixel slot k =======================
+    // ======================= builders: warps 8 + 2k, 9 + 2k own pixel slot k =======================
     const uint32_t slot = (uint32_t)(warp - TC_EPI_WARPS) >> 1;
     const uint32_t pt = (uint32_t)tid & 63u;
     const uint32_t esh = (uint32_t)(reinterpret_cast<uintptr_t>(a.bins) >> 1) & 7u;  // elements before 16 B alignment
     const uint4* gb = reinterpret_cast<const uint4*>(a.bins - esh);
-    // the photon range of (pixel p, round r): [b0, b1); this thread's groups of it
-    auto range = [&](long long p, uint32_t r, uint32_t& b0, uint32_t& b1) {
-      if (p < a.npix) {
-        const uint32_t o0 = a.offsets[p], o1 = a.offsets[p + 1];
-        b0 = o0 + r * CNT_MAX;
-        b1 = min(o1, b0 + CNT_MAX);
-        if (b0 > b1) b0 = b1;
-      } else {
-        b0 = b1 = 0;
-      }
+    // the photon range [b0, b1) of this slot's pixel of local tile lt, round r
+    auto range = [&](uint32_t lt, uint32_t r, uint32_t& b0, uint32_t& b1) {
+      const uint32_t o0 = so[4 * lt + slot], o1 = so[4 * lt + slot + 1];
+      b0 = min(o0 + r * CNT_MAX, o1);
+      b1 = min(o1, b0 + CNT_MAX);
     };
-    auto load_groups = [&](uint32_t b0, uint32_t b1, uint4 (&v)[PF]) {
+    auto load_groups = [&](uint32_t lt, uint32_t r, uint4 (&v)[PF]) {
+      uint32_t b0, b1;
+      range(lt, r, b0, b1);
       const uint32_t G0 = (b0 + esh) >> 3, G1 = (b1 + esh + 7u) >> 3;
 #pragma unroll
       for (int g = 0; g < PF; g++) {
@@ -227,86 +250,102 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
         v[g] = (b0 < b1 && G < G1) ? __ldg(gb + G) : make_uint4(0u, 0u, 0u, 0u);
       }
     };
-    // rounds of a tile: the largest pixel count of its 4 pixels, in CNT_MAX units
-    auto tile_rounds = [&](long long t) -> uint32_t {
-      uint32_t mx = 0;
-      for (int k = 0; k < 4; k++) {
-        const long long p = 4 * t + k;
-        if (p < a.npix) mx = max(mx, a.offsets[p + 1] - a.offsets[p]);
-      }
-      return mx == 0 ? 1u : (mx + CNT_MAX - 1) / CNT_MAX;
-    };
-    long long t = blockIdx.x;
-    uint32_t b0 = 0, b1 = 0, nb0 = 0, nb1 = 0;
-    uint4 cur[PF], nxt[PF];
-    range(4 * t + slot, 0, b0, b1);
-    load_groups(b0, b1, cur);
-    uint32_t rounds = tile_rounds(t);
-    uint32_t unit = 0, lt = 0;
-    for (; t < ntiles; t += gridDim.x, lt++) {
-      const long long tn = t + gridDim.x;
-      const uint32_t rounds_n = tn < ntiles ? tile_rounds(tn) : 1u;
+    uint32_t unit = 0;
+    // one local tile: its rounds from `cur` (round 0 loaded two tiles earlier), tile lt + 2's
+    // first round issued into `dst` (the buffer of tile lt - 1, consumed)
+    auto body = [&](uint32_t lt, uint4 (&cur)[PF], uint4 (&dst)[PF]) {
+      const uint32_t rounds = rounds_s[lt];
       for (uint32_t r = 0; r < rounds; r++, unit++) {
         const uint32_t s = unit & 1u;
         unsigned char* Ab = A0 + s * ASZ + slot * SLOT_B;
-        if (r > 0) {  // heavy pixel rounds: this round's groups now
-          range(4 * t + slot, r, b0, b1);
-          load_groups(b0, b1, cur);
-        }
-        if (r + 1 == rounds && tn < ntiles) {  // next tile's first round, one tile ahead
-          range(4 * tn + slot, 0, nb0, nb1);
-          load_groups(nb0, nb1, nxt);
-        }
+        if (r > 0) load_groups(lt, r, cur);  // heavy pixel rounds: this round's groups now
+        if (r == 0 && lt + 2 < ntl) load_groups(lt + 2, 0, dst);
+        uint32_t b0, b1;
+        range(lt, r, b0, b1);
+#ifdef TC_PROF
+        const bool prof = tid == TC_EPI_WARPS * 32;
+        long long c0 = clock64(), c1 = c0, c2 = c0;
+#endif
         if (unit >= 2) {
           mbar_wait(&empty_bar[s], ((unit >> 1) - 1u) & 1u);  // MMAs of unit - 2 done with this stage
+#ifdef TC_PROF
+          c1 = clock64();
+#endif
           for (uint32_t e = pt; e < SLOT_B / 16; e += TC_SLOT_THREADS)
             reinterpret_cast<uint4*>(Ab)[e] = make_uint4(0u, 0u, 0u, 0u);
           asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(TC_SLOT_THREADS) : "memory");
         }
+#ifdef TC_PROF
+        c2 = clock64();
+#endif
         if (b0 < b1) {
-          const uint32_t G0 = (b0 + esh) >> 3;
-          const uint32_t lo = b0 + esh, hi = b1 + esh;  // element indices relative to the aligned base
+          const uint32_t G0 = (b0 + esh) >> 3, G1 = (b1 + esh + 7u) >> 3;
+          const int lo = (int)(b0 + esh), hi = (int)(b1 + esh);  // element indices relative to the aligned base
+          uint32_t* Aw = reinterpret_cast<uint32_t*>(Ab);
 #pragma unroll
           for (int g = 0; g < PF; g++) {
             const uint32_t G = G0 + pt + (uint32_t)g * TC_SLOT_THREADS;
-            const uint32_t w4[4] = {cur[g].x, cur[g].y, cur[g].z, cur[g].w};
+            if (G < G1) {
+              // the group's photons inside [lo, hi) as a bit mask (all 8 except at the range ends)
+              const int el = min(max(lo - (int)(8u * G), 0), 8), eh = min(max(hi - (int)(8u * G), 0), 8);
+              const uint32_t msk = (0xffu << el) & (0xffu >> (8 - eh));
+              const uint32_t w4[4] = {cur[g].x, cur[g].y, cur[g].z, cur[g].w};
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
-              const uint32_t gi = 8u * G + (uint32_t)e;
-              const uint32_t x = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
-              // x < T: an out-of-range bin (precondition violation) is the zero "absent photon" term
-              if (gi >= lo && gi < hi && x < T)
-                atomicAdd(reinterpret_cast<uint32_t*>(Ab + ((x << 1) & ~3u)), 1u << ((x & 1u) << 4));
+              for (int e = 0; e < 8; e++) {
+                const uint32_t x = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+                // x < T: an out-of-range bin (precondition violation) is the zero "absent photon"
+                // term (a zero increment at a wrapped in-block address)
+                const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
+                atomicAdd(Aw + ((x >> 1) & (SLOT_B / 4 - 1u)), inc);  // unconditional: a branch per photon costs more
+              }
             }
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#ifdef TC_PROF
+        if (prof) {
+          const long long c3 = clock64();
+          atomicAdd(&tc_prof[0], (unsigned long long)(c1 - c0));
+          atomicAdd(&tc_prof[1], (unsigned long long)(c2 - c1));
+          atomicAdd(&tc_prof[2], (unsigned long long)(c3 - c2));
+          atomicAdd(&tc_prof[3], 1ull);
+        }
+#endif
         __syncwarp();
         if (tid == TC_EPI_WARPS * 32)
           uflags[s] = (r == 0 ? UF_FIRST : 0u) | (r + 1 == rounds ? UF_LAST : 0u) |
-                      (r + 1 == rounds && tn >= ntiles ? UF_END : 0u) | ((lt & 1u) ? UF_TB : 0u);
+                      (r + 1 == rounds && lt + 1 == ntl ? UF_END : 0u) | ((lt & 1u) ? UF_TB : 0u);
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_bar[s]);
       }
-      rounds = rounds_n;
-      b0 = nb0;
-      b1 = nb1;
-#pragma unroll
-      for (int g = 0; g < PF; g++) cur[g] = nxt[g];
+    };
+    uint4 q0[PF], q1[PF], q2[PF];
+    if (ntl > 0) load_groups(0, 0, q0);
+    if (ntl > 1) load_groups(1, 0, q1);
+    for (uint32_t lt = 0; lt < ntl; lt += 3) {
+      body(lt, q0, q2);
+      if (lt + 1 < ntl) body(lt + 1, q1, q0);
+      if (lt + 2 < ntl) body(lt + 2, q2, q1);
     }
   } else if (warp == TC_MMA_WARP) {
     // ======================= MMA issuer =======================
-    if (lane == 0) {
+    if (lane == 0 && ntl > 0) {
       // D f32, A/B f16, both K-major, N, M = 128
       const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint32_t sa0 = su32(A0), sb = su32(Bs);
       uint32_t lt = 0;
       for (uint32_t unit = 0;; unit++) {
         const uint32_t s = unit & 1u;
+        TCP_T0
         mbar_wait(&full_bar[s], (unit >> 1) & 1u);
+        TCP_ADD(4, _tcp0);
         const uint32_t f = uflags[s];
         const uint32_t tb = (f & UF_TB) ? 1u : 0u;
+#ifdef TC_PROF
+        const long long _tcp1 = clock64();
+#endif
         if ((f & UF_FIRST) && lt >= 2) mbar_wait(&accempty_bar[tb], ((lt >> 1) - 1u) & 1u);
+        TCP_ADD(5, _tcp1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sa = sa0 + s * ASZ;
         for (uint32_t kk = 0; kk < Kb / 16; kk++)  // K step of 16 = two core matrices along K
@@ -321,20 +360,29 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
       }
     }
   } else {
-    // ======================= epilogue =======================
-    constexpr int NV = 2 * MP;
+    // ======================= epilogue: warp w = pixel slot w % 4, frequencies [MP/2 (w/4), MP/2 (w/4 + 1)) ====
+    constexpr int NF = MP / 2;       // frequencies of this warp
+    constexpr int NV = 2 * NF;       // values (re, im) reduced over the 32 rows: one per lane at MP = 32
+    const uint32_t eslot = (uint32_t)warp & 3u, half = (uint32_t)warp >> 2, jj0 = half * NF;
+    float2 wr[NF];  // this lane's (row a) twiddles for the warp's frequencies, held for the whole launch
+#pragma unroll
+    for (int jj = 0; jj < NF; jj++) wr[jj] = Ws[(jj0 + jj) * 32 + lane];
     uint32_t lt = 0;
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+    for (; lt < ntl; lt++) {
       const uint32_t tb = lt & 1u;
-      const long long p = 4 * t + warp;
-      uint32_t n = 0;
-      if (p < a.npix) n = a.offsets[p + 1] - a.offsets[p];
+      const long long p = p0 + 4 * lt + eslot;
+      const uint32_t n = so[4 * lt + eslot + 1] - so[4 * lt + eslot];
+      TCP_T0
       mbar_wait(&accfull_bar[tb], (lt >> 1) & 1u);
+      if (warp == 0 && lane == 0) TCP_ADD(6, _tcp0);
+#ifdef TC_PROF
+      const long long _tcp1 = clock64();
+#endif
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t base = tmem + tb * (uint32_t)N + ((uint32_t)(warp * 32) << 16);
+      const uint32_t base = tmem + tb * (uint32_t)N + ((eslot * 32u) << 16) + jj0;
       float acc[NV];
 #pragma unroll
-      for (int g = 0; g < MP / 8; g++) {
+      for (int g = 0; g < NF / 8; g++) {
         float ch[8], sh[8], cl[8], sl[8];
         tmem_ld8(base + 0 * MP + 8 * g, ch);
         tmem_ld8(base + 1 * MP + 8 * g, sh);
@@ -346,7 +394,7 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
           const int jj = 8 * g + k;
           const float pc = fmaf(cl[k], 0.000244140625f, ch[k]);  // hi + 2^-12 lo
           const float ps = fmaf(sl[k], 0.000244140625f, sh[k]);
-          const float2 w = Ws[jj * 32 + lane];
+          const float2 w = wr[jj];
           acc[2 * jj] = fmaf(w.x, pc, -w.y * ps);
           acc[2 * jj + 1] = fmaf(w.x, ps, w.y * pc);
         }
@@ -354,9 +402,9 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&accempty_bar[tb]);
-      // reduce-scatter over the 32 rows a (lanes): lane l keeps value indices with its bits
+      // reduce-scatter over the 32 rows a (lanes): lane l keeps the value indices with its bits
 #pragma unroll
-      for (int o = 16, h = NV / 2; o >= 1; o >>= 1, h >>= 1) {
+      for (int o = 16, h = NV / 2; o >= 1 && h >= 1; o >>= 1, h >>= 1) {
         const bool up = (lane & o) != 0;
 #pragma unroll
         for (int i = 0; i < h; i++) {
@@ -365,13 +413,17 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1) sketch_tc_kernel(SketchArgs
           acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
       }
-      if (p < a.npix) {
+      if constexpr (NV == 16) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+      if (warp == 0 && lane == 0) TCP_ADD(7, _tcp1);
+      if (p < pend) {
         const float sc = n ? (float)(16777216.0 / (double)n) : 0.f;  // 2^24 (count encoding) / n
-        float2* zp = reinterpret_cast<float2*>(a.z) + (size_t)p * a.mstride + a.j0;
-        if constexpr (MP == 32) {
-          if ((uint32_t)lane < M) zp[lane] = make_float2(acc[0] * sc, acc[1] * sc);
+        float* zp = reinterpret_cast<float*>(reinterpret_cast<float2*>(a.z) + (size_t)p * a.mstride + a.j0 + jj0);
+        if constexpr (NV == 32) {
+          // lane l holds value index l: frequency jj0 + l / 2, component l % 2
+          if (jj0 + ((uint32_t)lane >> 1) < M) zp[lane] = acc[0] * sc;
         } else {
-          if ((uint32_t)(lane >> 1) < M) reinterpret_cast<float*>(zp)[lane] = acc[0] * sc;
+          // NV = 16: lanes l and l ^ 1 hold value index l / 2 (frequency jj0 + l / 4, component (l / 2) % 2)
+          if (!(lane & 1) && jj0 + ((uint32_t)lane >> 2) < M) zp[lane >> 1] = acc[0] * sc;
         }
       }
     }
@@ -388,19 +440,27 @@ cudaError_t launch_tc_t(const SketchArgs& a, uint32_t M, cudaStream_t s, int num
   static SmemAttrOnce attr;
   cudaError_t e = smem_attr_once(attr, fn, (int)sketch_tc_smem(TC_MAX_T, MP));
   if (e != cudaSuccess) return e;
-  const long long tiles = (a.npix + 3) / 4;
-  long long grid = num_sms;  // one persistent CTA per SM (shared memory, TMEM)
-  if (grid > tiles) grid = tiles;
-  if (grid < 1) grid = 1;
-  fn<<<(unsigned)grid, TC_THREADS_ALL, sketch_tc_smem(a.T, MP), s>>>(a, M);
-  return cudaGetLastError();
+  // one persistent CTA per SM (shared memory, TMEM), each a contiguous run of <= TC_TPC_MAX tiles
+  // (its offsets staged in shared memory); frames beyond num_sms * TC_TPC_MAX tiles take several launches
+  const long long per_launch = 4ll * TC_TPC_MAX * num_sms;
+  for (long long pb = 0; pb < a.npix; pb += per_launch) {
+    const long long pc = min(per_launch, a.npix - pb);
+    const long long tiles = (pc + 3) / 4;
+    const long long tpc = (tiles + num_sms - 1) / num_sms;
+    const long long grid = (tiles + tpc - 1) / tpc;
+    fn<<<(unsigned)grid, TC_THREADS_ALL, sketch_tc_smem(a.T, MP), s>>>(a, M, pb, pc, (uint32_t)tpc);
+    cudaError_t e2 = cudaGetLastError();
+    if (e2 != cudaSuccess) return e2;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
 
 size_t sketch_tc_smem(uint32_t T, int MP) {
   const size_t Kb = (size_t)1 << tc_log2_kb(T);
-  return 128 + 2 * 256 * Kb + (size_t)4 * MP * Kb * 2 + (size_t)MP * 32 * sizeof(float2);
+  return 128 + 2 * 256 * Kb + (size_t)4 * MP * Kb * 2 + (size_t)MP * 32 * sizeof(float2) +
+         sizeof(uint32_t) * (5 * (size_t)TC_TPC_MAX + 1);
 }
 
 cudaError_t launch_sketch_tc(int M, const SketchArgs& a, cudaStream_t s, int num_sms) {
@@ -410,3 +470,14 @@ cudaError_t launch_sketch_tc(int M, const SketchArgs& a, cudaStream_t s, int num
 }
 
 }  // namespace srt3d
+
+#ifdef TC_PROF
+extern "C" int srt3d_debug_tc_prof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, srt3d::tc_prof, sizeof(srt3d::tc_prof)) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(srt3d::tc_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
