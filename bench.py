@@ -335,13 +335,41 @@ def time_grad(torch, srt3d, z, t0, a0, sigma, T, m, iters, s, flush, reps=20):
 
 def sketch_work(srt3d, npix, T, m, n_photons):
     """Algorithmic bytes and flops of one sketch launch (SURVEY §8(d)): B = 2n + 4(npix+1) + 8 m npix;
-    F = 8 m n for the direct sum (direct / routed / paired paths), 8 m T npix for the bin-count path."""
+    F = 8 m n for the direct sum (direct / routed / paired / tensor-core paths: the problem's FP32 count,
+    whatever unit executes it), 8 m T npix for the bin-count path."""
     path, lanes = srt3d.srt3d_sketch_plan(npix, T, m, n_photons)
     b = 2.0 * n_photons + 4.0 * (npix + 1) + 8.0 * m * npix
     f = 8.0 * m * (T * npix if path == srt3d.PATH_BINCOUNT else n_photons)
-    name = {srt3d.PATH_DIRECT: "direct", srt3d.PATH_PAIRED: "paired", srt3d.PATH_ROUTED: "routed"}.get(path,
-                                                                                                   "bincount")
+    name = {srt3d.PATH_DIRECT: "direct", srt3d.PATH_PAIRED: "paired", srt3d.PATH_ROUTED: "routed",
+            srt3d.PATH_TENSOR: "tensor"}.get(path, "bincount")
     return path, lanes, name, b, f
+
+
+def tc_gemm_flops(npix, T, m):
+    """Tensor-core flops one tensor-path sketch launch executes: per pass of M <= 32
+    frequencies, a [4 x 32 rows, Kb] x [Kb, 4 MP] f16 GEMM per tile of 4 pixels (MP = 16 if M <= 16
+    else 32; Kb = the power of two >= T / 32, at least 16)."""
+    q = 4
+    while (32 << q) < T:
+        q += 1
+    f = 0.0
+    for j0 in range(0, m, 32):
+        mp = 16 if min(32, m - j0) <= 16 else 32
+        f += 2.0 * ((npix + 3) // 4 * 4) * 32 * (1 << q) * 4 * mp
+    return f
+
+
+def tensor_roofline(peaks, npix, T, m, ms):
+    """The tensor-core sketch against the f16 dense peak (the measured bf16 peak: the same rate)."""
+    f = tc_gemm_flops(npix, T, m)
+    pk = float(peaks.get("bf16_tflops", 1653.6)) * 1e12
+    t = ms * 1e-3
+    return {"kernel": "srt3d_sketch (tensor path)", "bound": "tensor", "achieved": f / t / 1e12, "peak": pk / 1e12,
+            "unit": "TFLOP/s", "frac": f / pk / t, "executed_tensor_flops_per_launch": f,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (f16 dense: same rate)",
+            "note": "tcgen05 kind::f16 histogram x DFT-block GEMM incl. the hi/lo split of V; the kernel is "
+                    "bound by shared-memory wavefronts (histogram zeroing + atomics + MMA operand reads: ~97% of "
+                    "the 1/clk/SM port in profiles/r02_ncu_tc_C5.json), not by the tensor pipe"}
 
 
 def grad_work(npix, m, K, loss=False):
@@ -385,6 +413,8 @@ def run_sweep(args, torch, srt3d, roofline, s, l2_bytes):
                           "input larger than L2 (not flushed)",
                           "roofline_median": roofline("srt3d_sketch", b, fl, med),
                           "roofline_min": roofline("srt3d_sketch", b, fl, mn),
+                          "roofline_tensor_median": (tensor_roofline(load_peaks()[0], fr.npix, fr.T, fr.m, med)
+                                                     if path == srt3d.PATH_TENSOR else None),
                           "traffic": traffic.get(fr.name, {}).get("srt3d_sketch")}}
         if fr.iters:
             t0, a0 = (torch.from_numpy(x).cuda() for x in fr.theta0())
@@ -618,6 +648,12 @@ def run_srt3d(args):
               "roofline_min": roofline("srt3d_sketch", sk_bytes, sk_flops, sk_rep[1]),
               "fp32_measured_tflops": fp32_meas / 1e12 if fp32_meas else None,
               "frac_of_measured_fp32": (sk_flops / (sk_avg * 1e-3)) / fp32_meas if fp32_meas else None}
+    if path == srt3d.PATH_TENSOR:
+        sketch["roofline_tensor"] = tensor_roofline(peaks, f.npix, f.T, f.m, sk_avg)
+        sketch["roofline_note"] = ("roofline: the north-star definition (slower of bytes at HBM peak and the direct "
+                                   "sum's 8 m n flops at FP32 peak); above 1 because the tensor-core path evaluates "
+                                   "the sum as a GEMM on the binned photons; roofline_tensor: the executed GEMM vs "
+                                   "the f16 tensor peak")
     grad = None
     if f.iters > 0:
         per_iter = it_avg / f.iters

@@ -104,6 +104,8 @@ cudaError_t launch_regime(uint32_t rg, int M, const srt3d::SketchArgs& a, cudaSt
       return srt3d::launch_sketch_pass(M, srt3d::SK_G4_CHEB, a, s, nsm);
     case srt3d::RG_RT:
       return srt3d::launch_sketch_routed(M, a, s, nsm);
+    case srt3d::RG_TC:
+      return srt3d::launch_sketch_tc(M, a, s, nsm);
     case srt3d::RG_H128:
       return srt3d::launch_sketch_hist(M, a, 128, s, nsm);
     case srt3d::RG_H256:
@@ -120,7 +122,7 @@ cudaError_t launch_regime(uint32_t rg, int M, const srt3d::SketchArgs& a, cudaSt
 // breakpoints at these means, so evaluating it there finds every candidate.
 int regime_candidates(int64_t npix, uint32_t T, int M, uint32_t mode, uint32_t j0, uint32_t* out) {
   const unsigned long long np = (unsigned long long)npix;
-  const unsigned long long means[] = {0, 256, 2048, 4096, T, 30000, 80000};
+  const unsigned long long means[] = {0, 256, 2048, 4096, T, srt3d::TC_MAX_MEAN_PER_T * T, 30000, 80000};
   int n = 0;
   for (unsigned long long mu : means) {
     const unsigned long long tot = mu * np;
@@ -236,7 +238,10 @@ int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photo
   const uint32_t rg = srt3d::sketch_regime(total_photons, npix, T, M0,
                                            hist_fits(T, M0) ? srt3d::RGM_AUTO : srt3d::RGM_DIRECT, 0);
   if (lanes_per_pixel) *lanes_per_pixel = regime_lanes(rg);
-  return rg >= srt3d::RG_H128 ? SRT3D_PATH_BINCOUNT : rg == srt3d::RG_RT ? SRT3D_PATH_ROUTED : SRT3D_PATH_DIRECT;
+  return rg >= srt3d::RG_H128 ? SRT3D_PATH_BINCOUNT
+         : rg == srt3d::RG_RT ? SRT3D_PATH_ROUTED
+         : rg == srt3d::RG_TC ? SRT3D_PATH_TENSOR
+                              : SRT3D_PATH_DIRECT;
 }
 
 int srt3d_expected_sketch(const float* t, const float* alpha, int64_t npix, uint32_t K, float sigma, uint32_t T,

@@ -50,13 +50,14 @@ struct SketchArgs {
 // A function of the frame's photon count, evaluated with exact integer
 // comparisons so the host (with a hint) and the device (from offsets) agree:
 // mean >= X  <=>  total >= X * npix.
-enum : uint32_t { RG_NONE = 0, RG_G4, RG_G8, RG_G16, RG_G32, RG_G4C, RG_RT, RG_H128, RG_H256, RG_H512, RG_COUNT };
+enum : uint32_t { RG_NONE = 0, RG_G4, RG_G8, RG_G16, RG_G32, RG_G4C, RG_RT, RG_TC, RG_H128, RG_H256, RG_H512, RG_COUNT };
 // class-routed Chebyshev kernel (sketch_routed.cu): first pass only, T % 4 == 0, T <= RT_MAX_T
 constexpr uint32_t RT_MAX_T = 12000;  // 1.25 T phasor entries + T class bytes + [32][512] fp32 partials + spills <= 227 KB
 __host__ __device__ inline bool routed_fits(uint32_t T, uint32_t j0) { return j0 == 0 && T % 4 == 0 && T <= RT_MAX_T; }
-// tensor-core sketch (sketch_tc.cu): Kb = 64 ceil(T / 2048) <= 256 columns per row, R = ceil(T / Kb) <= 32 rows
+// tensor-core sketch (sketch_tc.cu): a pixel's bins fill a 32 x Kb fp16 block, Kb = 2^q <= 256
 constexpr uint32_t TC_MAX_T = 8192;
 __host__ __device__ inline bool tc_fits(uint32_t T) { return T >= 1 && T <= TC_MAX_T; }
+constexpr unsigned long long TC_MAX_MEAN_PER_T = 3;  // AUTO: tensor-core path below 3 T photons per pixel (measured)
 enum : uint32_t { RGM_AUTO = 0, RGM_DIRECT = 1, RGM_HIST = 2 };
 constexpr uint32_t SK_TABLE_MAX_T = 24575;  // (T + 1) float2 entries fit SK_MAX_SMEM
 // mode: RGM_AUTO (bin-count allowed: the host passes it only when the
@@ -64,6 +65,9 @@ constexpr uint32_t SK_TABLE_MAX_T = 24575;  // (T + 1) float2 entries fit SK_MAX
 __host__ __device__ inline uint32_t sketch_regime(unsigned long long total, long long npix, uint32_t T, int M,
                                                   uint32_t mode, uint32_t j0) {
   const unsigned long long np = npix > 0 ? (unsigned long long)npix : 1ull;
+  // tensor-core sketch (§5.7): measured fastest at every BASELINE config with T <= 8192 and a mean
+  // below 3 T photons per pixel (above it the bin-count path's HBM-bound histogram wins)
+  if (mode == RGM_AUTO && tc_fits(T) && total < TC_MAX_MEAN_PER_T * T * np) return RG_TC;
   const bool hist = mode == RGM_HIST || (mode == RGM_AUTO && total >= (unsigned long long)T * np);
   if (hist) {
     if (total < 30000ull * np) return RG_H128;  // CTA size by photons per pixel (tools/hist_tune.cu)

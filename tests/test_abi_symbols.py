@@ -97,3 +97,21 @@ def test_host_validation_without_gpu():
     assert lib.srt3d_descent_update(dummy, dummy, dummy, dummy, 4, 2, ctypes.c_float(1.0), 100, 3,
                                     ctypes.c_float(-1.0), None) == -1
     assert b"eta" in lib.srt3d_last_error()
+
+
+def test_sketch_plan_regimes_without_gpu():
+    """srt3d_sketch_plan (host only) picks the measured-fastest regime per BASELINE config
+    (DESIGN.md §5.7): the tensor-core path below 3 T photons per pixel at T <= 8192, the bin-count
+    path above it, the routed direct path where T > 8192 (it then fits up to 12000)."""
+    import paper_2203_00952_b200 as p
+
+    plan = lambda npix, T, m, tot: p.srt3d_sketch_plan(npix, T, m, tot)[0]  # noqa: E731
+    assert plan(262144, 8192, 32, 262121072) == p.PATH_TENSOR              # C5
+    assert plan(1024, 1024, 4, 51200) == p.PATH_TENSOR                      # C1
+    assert plan(19881, 4613, 10, 19881 * 1000) == p.PATH_TENSOR            # C2
+    assert plan(65536, 2500, 20, 65536 * 10000) == p.PATH_BINCOUNT         # C3: 4 T per pixel
+    assert plan(4096, 4096, 10, 4096 * 10000) == p.PATH_TENSOR              # C4@1e4: 2.4 T
+    assert plan(4096, 4096, 10, 4096 * 100000) == p.PATH_BINCOUNT           # C4@1e5
+    assert plan(4096, 8192, 10, 4096 * (3 * 8192) - 1) == p.PATH_TENSOR     # just below 3 T
+    assert plan(4096, 8192, 10, 4096 * (3 * 8192)) == p.PATH_BINCOUNT
+    assert plan(4096, 8196, 32, 4096 * 1000) == p.PATH_ROUTED               # T > 8192

@@ -121,7 +121,7 @@ def test_out_of_range_bins_finite_on_every_path(gpu, oracle_mod, T):
     calls = [dict(), dict(total_photons=int(offs[-1]))]
     calls += [dict(path=gpu.PATH_DIRECT, lanes_per_pixel=g, total_photons=int(offs[-1])) for g in (4, 8, 16, 32)]
     calls += [dict(path=gpu.PATH_BINCOUNT), dict(path=gpu.PATH_PAIRED), dict(path=gpu.PATH_DIRECT),
-              dict(path=gpu.PATH_ROUTED), dict(path=gpu.PATH_ROUTED, lanes_per_pixel=2)]
+              dict(path=gpu.PATH_ROUTED), dict(path=gpu.PATH_ROUTED, lanes_per_pixel=2), dict(path=gpu.PATH_TENSOR)]
     for kw in calls:
         if "path" in kw:
             z = gpu.srt3d_sketch_ex(db, do, T, 32, **kw)

@@ -47,6 +47,8 @@ def test_fuzz_sketch_paths(gpu, oracle_mod, inputs_mod, i):
         regimes.append((gpu.PATH_PAIRED, 0))
     if T % 4 == 0 and T <= 12000:
         regimes.append((gpu.PATH_ROUTED, 0))
+    if T <= 8192:
+        regimes.append((gpu.PATH_TENSOR, 0))
     for path, lanes in regimes:
         try:
             z = gpu.srt3d_sketch_ex(db, do, T, m, total_photons=int(offs[-1]), path=path, lanes_per_pixel=lanes)

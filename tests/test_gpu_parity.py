@@ -234,6 +234,38 @@ def test_sketch_class_paths_alignment_and_determinism(gpu, oracle_mod, inputs_mo
         gpu.srt3d_sketch_ex(db, do, {4: 12004, 5: 8193}.get(path, 23801), m, path=path, lanes_per_pixel=lanes)
 
 
+@pytest.mark.parametrize("T,m", [(4096, 10), (8192, 32), (1000, 20)])
+def test_sketch_tensor_heavy_pixels(gpu, oracle_mod, T, m):
+    """Tensor-core path on pixels past one round (> 2040 photons: counts are
+    encoded as fp16 bit patterns < 2048, so a heavy tile runs several rounds accumulating into the
+    same TMEM columns): 1e5 photons in one bin (the largest count per bin, every round's error in the
+    same direction), 1e5 uniform photons, the round boundaries 2040 / 2041 / 4081, an empty pixel."""
+    import torch
+
+    rng = np.random.default_rng(T + m)
+    lists = [[T // 3] * 100000, list(rng.integers(0, T, 100000)), list(rng.integers(0, T, 2040)),
+             list(rng.integers(0, T, 2041)), [T - 1] * 4081, [], list(rng.integers(0, T, 7))]
+    bins, offs = _csr(lists)
+    z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, m, total_photons=int(offs[-1]), path=gpu.PATH_TENSOR)
+    torch.cuda.synchronize()
+    _assert_sketch_close(_host(z), oracle_mod.sketch(bins, offs, T, m))
+
+
+def test_sketch_tensor_multi_launch_split(gpu, oracle_mod, inputs_mod):
+    """A frame beyond one launch of the tensor-core kernel (768 tiles of 4 pixels per CTA, offsets
+    staged in shared memory): the launcher splits it, every pixel is computed once."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    npix = 4 * 768 * sms + 4 * 37 + 3
+    bins, offs = inputs_mod.random_csr(npix=npix, T=1024, max_n=3, seed=11)
+    z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), 1024, 4, total_photons=int(offs[-1]), path=gpu.PATH_TENSOR)
+    torch.cuda.synchronize()
+    zg = _host(z)
+    _assert_sketch_close(zg, oracle_mod.sketch(bins, offs, 1024, 4))
+    assert np.all(zg[np.diff(offs.astype(np.int64)) == 0] == 0)
+
+
 def test_sketch_alignment_and_offsets_base(gpu, oracle_mod):
     """Segments starting at every residue mod 8, n = 0..17, non-zero offsets[0], odd bins base."""
     import torch
