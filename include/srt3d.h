@@ -108,12 +108,13 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  *                   is enqueued; SRT3D_HINT_UNKNOWN (0) selects on the device
  *                   as srt3d_sketch does.  A wrong hint changes the launch
  *                   shape only, never the result.
- *   path            SRT3D_PATH_AUTO (0): bin-count when the mean photon count
- *                   per pixel is >= SRT3D_BINCOUNT_MIN_PHOTONS_PER_BIN * T and
- *                   the histogram fits in shared memory; else ROUTED for a
- *                   first pass of >= 24 frequencies at 256..2047 photons per
- *                   pixel where it applies; else direct (AUTO never selects
- *                   PAIRED: measured slower);
+ *   path            SRT3D_PATH_AUTO (0): TENSOR when T <= 8192 and the mean
+ *                   photon count per pixel is below 3 T; else bin-count when
+ *                   the mean is >= T and the histogram fits in shared memory;
+ *                   else ROUTED for a first pass of >= 24 frequencies at
+ *                   256..2047 photons per pixel where it applies; else direct
+ *                   (AUTO never selects PAIRED: measured slower, DESIGN.md
+ *                   §5.1);
  *                   SRT3D_PATH_DIRECT (1): per-photon recurrence,
  *                   lanes_per_pixel lanes per pixel (0: by the photon count);
  *                   SRT3D_PATH_BINCOUNT (2): per-pixel shared-memory
@@ -134,7 +135,16 @@ int srt3d_sketch(const uint16_t* bins, const uint32_t* offsets, int64_t npix, ui
  *                   T % 4 == 0 and T <= 12000, else SRT3D_EUNSUPPORTED;
  *                   passes after the first 32 frequencies run the direct
  *                   path).
- *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path); 0 or 2 (routed).
+ *                   SRT3D_PATH_TENSOR (5): the bin-count sum on the tensor
+ *                   cores: each pixel's photons are counted into a 32 x Kb
+ *                   shared-memory histogram (Kb = 2^q >= T / 32) whose counts
+ *                   are fed as fp16 bit patterns, multiplied on tcgen05 by the
+ *                   per-column phasors e^{i w_j X_col} (hi + lo fp16 split),
+ *                   and the 32 row sums twiddled by e^{i w_j X_row} and added
+ *                   (T <= 8192, else SRT3D_EUNSUPPORTED; any
+ *                   photon count: pixels above 2040 photons run in rounds).
+ *   lanes_per_pixel 0 (auto) or 4, 8, 16, 32 (direct path); 0 or 2 (routed);
+ *                   0 (tensor).
  * Errors as srt3d_sketch, plus SRT3D_EINVAL for an unknown path or lane count.
  */
 #define SRT3D_PATH_AUTO 0
@@ -150,11 +160,12 @@ int srt3d_sketch_ex(const uint16_t* bins, const uint32_t* offsets, int64_t npix,
 
 /*
  * srt3d_sketch_plan — host-only query: the path (SRT3D_PATH_DIRECT,
- * SRT3D_PATH_BINCOUNT or SRT3D_PATH_ROUTED) and lanes per pixel srt3d_sketch
+ * SRT3D_PATH_BINCOUNT, SRT3D_PATH_ROUTED or SRT3D_PATH_TENSOR) and lanes per pixel srt3d_sketch
  * would use for the first 32-frequency pass of a frame of npix pixels and
  * total_photons photons.  Returns the path (> 0) or a negative error code;
  * *lanes_per_pixel (may be NULL) receives the lane count (0 for the
- * bin-count path, which uses one CTA per pixel; 2 for the routed path).
+ * bin-count path, which uses one CTA per pixel, and for the tensor-core path,
+ * a warp pair per pixel slot of a 4-pixel tile; 2 for the routed path).
  */
 int srt3d_sketch_plan(int64_t npix, uint32_t T, uint32_t m, uint64_t total_photons, int* lanes_per_pixel);
 
