@@ -369,7 +369,7 @@ def tensor_roofline(peaks, npix, T, m, ms):
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (f16 dense: same rate)",
             "note": "tcgen05 kind::f16 histogram x DFT-block GEMM incl. the hi/lo split of V; the kernel is "
                     "bound by shared-memory wavefronts (histogram zeroing + atomics + MMA operand reads: ~97% of "
-                    "the 1/clk/SM port in profiles/r02_ncu_tc_C5.json), not by the tensor pipe"}
+                    "the 1/clk/SM port in profiles/r02_sketch_tc_ncu_C5.json), not by the tensor pipe"}
 
 
 def grad_work(npix, m, K, loss=False):

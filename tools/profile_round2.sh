@@ -12,7 +12,7 @@ python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-init --no-s
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-init --no-stream --no-sweep > $O/ncu_launch.log 2>&1
 python tools/launch_summary.py $O/launches_c5.csv $P/r02_launches_c5.json > /dev/null
-K='sketch_kernel|sketch_routed|sketch_hist|grad_kernel|fit_kernel|bp_tc_kernel|backproject_kernel|init_k1|merge_kernel'
+K='sketch_kernel|sketch_routed|sketch_tc|sketch_hist|grad_kernel|fit_kernel|bp_tc_kernel|backproject_kernel|init_k1|merge_kernel'
 for c in C5 C3 C2 C1; do
   python tools/prof_kernels.py $c --iters 1 --next > $O/pre_$c.log 2>&1 || exit 1
   ncu --set full --clock-control none --import-source on -k regex:"$K" --launch-skip 0 --launch-count 12 \

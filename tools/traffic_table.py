@@ -6,7 +6,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ENTRY = [("sketch_routed", "srt3d_sketch"), ("sketch_hist", "srt3d_sketch"), ("sketch_kernel", "srt3d_sketch"),
+ENTRY = [("sketch_tc", "srt3d_sketch"), ("sketch_routed", "srt3d_sketch"), ("sketch_hist", "srt3d_sketch"), ("sketch_kernel", "srt3d_sketch"),
          ("grad_kernel", "srt3d_sketch_grad_step"), ("fit_kernel", "srt3d_fit_pixelwise"),
          ("bp_tc_kernel", "srt3d_init_depths"), ("init_k1", "srt3d_init_k1"), ("merge_kernel", "srt3d_sketch_merge")]
 
