@@ -78,6 +78,23 @@ __device__ __forceinline__ uint64_t ns_desc(uint32_t saddr, uint32_t sbo) {
   return d;
 }
 
+#ifndef TC_CP
+// 1: each histogram stage copied into TMEM (tcgen05.cp 128x256b) and multiplied from there (A in
+// TMEM: 98 instead of 127 cycles per MMA in isolation, microbench/umma_rate.cu).  Measured slower in
+// the kernel: C5 0.91 vs 0.68 ms (the TMEM writes contend with the epilogue's TMEM reads); off.
+#define TC_CP 0
+#endif
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bd, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
   float2* Ws = reinterpret_cast<float2*>(Bs + (size_t)N * Kb * 2u);  // [MP][32] (frequency-major)
   uint32_t* so = reinterpret_cast<uint32_t*>(Ws + MP * 32);            // this CTA's offsets [4 ntl + 1]
   uint32_t* rounds_s = so + 4 * TC_TPC_MAX + 1;                         // rounds per local tile [ntl]
-  __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], accfull_bar[2], accempty_bar[2];
+  __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], accfull_bar[2], accempty_bar[2], afree_bar[2];
   __shared__ uint32_t tmem_slot, uflags[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -214,12 +231,13 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
       mbar_init(&empty_bar[s], 1);
       mbar_init(&accfull_bar[s], 1);
       mbar_init(&accempty_bar[s], TC_EPI_WARPS);
+      mbar_init(&afree_bar[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
-                 "r"(2u * N));
+                 "r"(TC_CP ? 512u : 2u * N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -344,14 +362,31 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
 #ifdef TC_PROF
         const long long _tcp1 = clock64();
 #endif
+        const uint32_t sa = sa0 + s * ASZ;
+#if TC_CP
+        // the stage into TMEM columns 256 + 128 s (after the MMAs of unit - 2 read them), the stage
+        // released as soon as the copies land, then the MMAs with A in TMEM (98 vs 127 cycles each,
+        // microbench/umma_rate.cu)
+        const uint32_t ta = tmem + 256u + 128u * s;
+        if (unit >= 2) mbar_wait(&afree_bar[s], ((unit >> 1) - 1u) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (uint32_t kk = 0; kk < Kb / 16; kk++) cp_128x256b(ta + kk * 8u, ns_desc(sa + kk * 256u, SBO));
+        commit(&empty_bar[s]);
+#endif
         if ((f & UF_FIRST) && lt >= 2) mbar_wait(&accempty_bar[tb], ((lt >> 1) - 1u) & 1u);
         TCP_ADD(5, _tcp1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = sa0 + s * ASZ;
+#if TC_CP
+        for (uint32_t kk = 0; kk < Kb / 16; kk++)
+          mma_f16_ts(tmem + tb * (uint32_t)N, ta + kk * 8u, ns_desc(sb + kk * 256u, SBO), idesc,
+                     (!(f & UF_FIRST) || kk > 0) ? 1u : 0u);
+        commit(&afree_bar[s]);
+#else
         for (uint32_t kk = 0; kk < Kb / 16; kk++)  // K step of 16 = two core matrices along K
           mma_f16(tmem + tb * (uint32_t)N, ns_desc(sa + kk * 256u, SBO), ns_desc(sb + kk * 256u, SBO), idesc,
                   (!(f & UF_FIRST) || kk > 0) ? 1u : 0u);
         commit(&empty_bar[s]);
+#endif
         if (f & UF_LAST) {
           commit(&accfull_bar[tb]);
           lt++;
@@ -431,7 +466,8 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N));
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_CP ? 512u : 2u * N));
 }
 
 template <int MP>
