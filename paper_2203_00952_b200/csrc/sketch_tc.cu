@@ -146,6 +146,17 @@ __host__ __device__ inline uint32_t tc_log2_kb(uint32_t T) {
 __host__ __device__ inline uint32_t tc_xrow(uint32_t a, uint32_t q) { return ((a >> 3) << (q + 3)) + ((a & 7u) << 3); }
 __host__ __device__ inline uint32_t tc_xcol(uint32_t k) { return ((k >> 3) << 6) + (k & 7u); }
 
+// a 16-byte photon group at aligned element index e0, only its elements inside [flo, fhi)
+__device__ __noinline__ uint4 load_group_checked(const uint4* gp, uint32_t e0, uint32_t flo, uint32_t fhi) {
+  if (e0 >= flo && e0 + 8u <= fhi) return __ldg(gp);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  const uint16_t* e16 = reinterpret_cast<const uint16_t*>(gp);
+#pragma unroll
+  for (uint32_t e = 0; e < 8; e++)
+    if (e0 + e >= flo && e0 + e < fhi) w[e >> 1] |= (uint32_t)__ldg(e16 + e) << ((e & 1u) * 16);
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 #ifdef TC_PROF
 // tools-only timing build (SRT3D_EXTRA=-DTC_PROF): per-role cycle counters summed over CTAs
 __device__ unsigned long long tc_prof[16];
@@ -258,14 +269,25 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
       b0 = min(o0 + r * CNT_MAX, o1);
       b1 = min(o1, b0 + CNT_MAX);
     };
+    // the frame's photon range [offsets[0], offsets[npix]) in aligned element coordinates: a 16-byte
+    // group straddling either end is read element by element (the header's promise: no read outside
+    // it); only a pixel range starting in the frame's first or ending in its last group meets one
+    const uint32_t flo = a.offsets[0] + esh, fhi = a.offsets[a.npix] + esh;
     auto load_groups = [&](uint32_t lt, uint32_t r, uint4 (&v)[PF]) {
       uint32_t b0, b1;
       range(lt, r, b0, b1);
       const uint32_t G0 = (b0 + esh) >> 3, G1 = (b1 + esh + 7u) >> 3;
+      if (8u * G0 >= flo && 8u * G1 <= fhi) {
 #pragma unroll
-      for (int g = 0; g < PF; g++) {
-        const uint32_t G = G0 + pt + (uint32_t)g * TC_SLOT_THREADS;
-        v[g] = (b0 < b1 && G < G1) ? __ldg(gb + G) : make_uint4(0u, 0u, 0u, 0u);
+        for (int g = 0; g < PF; g++) {
+          const uint32_t G = G0 + pt + (uint32_t)g * TC_SLOT_THREADS;
+          v[g] = (b0 < b1 && G < G1) ? __ldg(gb + G) : make_uint4(0u, 0u, 0u, 0u);
+        }
+      } else {
+        for (int g = 0; g < PF; g++) {
+          const uint32_t G = G0 + pt + (uint32_t)g * TC_SLOT_THREADS;
+          v[g] = (b0 < b1 && G < G1) ? load_group_checked(gb + G, 8u * G, flo, fhi) : make_uint4(0u, 0u, 0u, 0u);
+        }
       }
     };
     uint32_t unit = 0;
