@@ -152,7 +152,8 @@ __device__ __forceinline__ void tree_argmax32(const float (&x)[32], float& mx, i
   im = iy[0];
 }
 
-template <bool PICK>
+// KK: the pick count rounded up to 1, 2, 3, 4 or MAX_K (compile-time loop bounds and register arrays)
+template <bool PICK, int KK>
 __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
   extern __shared__ unsigned char tc_raw[];
   unsigned char* sm = tc_raw + ((1024u - (su32(tc_raw) & 1023u)) & 1023u);  // 1 KB aligned (swizzle atoms)
@@ -361,8 +362,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
       }
       // K rounds: combine the splits' local bests (largest g, then smallest n);
       // every split thread of a pixel keeps the same pick list
-      int pick[MAX_K];
-      float pg[MAX_K];
+      int pick[KK];
+      float pg[KK];
       int cnt = 0;
       for (uint32_t k = 0; k < a.K; k++) {
         const int buf = k & 1;
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
             if (live) {
               elig = cand[c * TC_M];
 #pragma unroll
-              for (int q = 0; q < MAX_K; q++)
+              for (int q = 0; q < KK; q++)
                 if (q < cnt) elig &= ~excl_bits(pick[q], D, N, c * 32);
             }
             if (!__any_sync(0xffffffffu, elig != 0u)) continue;
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
         }
         if (cnt == (int)k && gi >= 0) {
 #pragma unroll
-          for (int q = 0; q < MAX_K; q++)
+          for (int q = 0; q < KK; q++)
             if (q == cnt) {
               pick[q] = gi;
               pg[q] = gb;
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
       if (split == 0 && pix < a.npix) {
         // sort by depth (insertion sort on the register arrays: compile-time indices)
 #pragma unroll
-        for (int x = 1; x < MAX_K; x++)
+        for (int x = 1; x < KK; x++)
 #pragma unroll
           for (int y = x; y > 0; y--)
             if (y < cnt && pick[y - 1] > pick[y]) {
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
             }
         const double tfirst = cnt ? (double)pick[0] * (double)a.T / (double)N : 0.0;
 #pragma unroll
-        for (int k = 0; k < MAX_K; k++) {
+        for (int k = 0; k < KK; k++) {
           if (k >= (int)a.K) break;
           const size_t o = (size_t)pix * a.K + k;
           if (k < cnt) {
@@ -467,9 +468,13 @@ bool backproject_tc_supported(uint32_t N, uint32_t m) { return m <= 32 && N % 32
 
 cudaError_t launch_backproject_tc(const BpArgs& a, bool pick, cudaStream_t s, int num_sms) {
   if (a.npix <= 0) return cudaSuccess;
-  auto fn = pick ? bp_tc_kernel<true> : bp_tc_kernel<false>;
-  static SmemAttrOnce attr[2];
-  cudaError_t e = smem_attr_once(attr[pick], fn, (int)bp_tc_smem(512, pick));
+  const int kk = !pick ? 1 : a.K <= 1 ? 1 : a.K == 2 ? 2 : a.K == 3 ? 3 : a.K == 4 ? 4 : MAX_K;
+  const int vi = !pick ? 0 : kk == 1 ? 1 : kk == 2 ? 2 : kk == 3 ? 3 : kk == 4 ? 4 : 5;
+  void (*const fns[6])(const BpArgs) = {bp_tc_kernel<false, 1>, bp_tc_kernel<true, 1>, bp_tc_kernel<true, 2>,
+                                        bp_tc_kernel<true, 3>,  bp_tc_kernel<true, 4>, bp_tc_kernel<true, MAX_K>};
+  auto fn = fns[vi];
+  static SmemAttrOnce attr[6];
+  cudaError_t e = smem_attr_once(attr[vi], fn, (int)bp_tc_smem(512, pick));
   if (e != cudaSuccess) return e;
   const long long tiles = (a.npix + TC_M - 1) / TC_M;
   long long grid = num_sms;  // one persistent CTA per SM (the accumulator holds up to all 512 TMEM columns)
