@@ -29,12 +29,14 @@
 //    columns per tcgen05.ld.  Backprojection stages each 32 x 32 block through
 //    shared memory for row-contiguous stores; init_depths finds its split's
 //    candidates (g_n > 0, g_n > g_{n-1}, g_n >= g_{n+1}, circular; the split's
-//    boundary neighbours read from the adjacent chunks) and local best in one
-//    pass (candidate bit masks in shared memory, tree argmax per chunk), the
-//    four splits' bests are combined through shared memory, and each further
-//    pick re-reads the split's columns with the exclusion zones of the earlier
-//    picks as per-chunk bit masks — the oracle's rule and tie order (largest
-//    g, then smallest n).
+//    boundary neighbours read from the adjacent chunks) in one pass over TMEM
+//    (the next chunk's tcgen05.ld in flight while a chunk is scanned), keeping
+//    per-chunk candidate bit masks and the candidates' values (in increasing n)
+//    in shared memory; every pick round walks that list with the exclusion
+//    zones of the earlier picks as per-chunk bit masks, the four splits' bests
+//    are combined through shared memory — the oracle's rule and tie order
+//    (largest g, then smallest n).  A thread whose list would overflow re-reads
+//    TMEM in its rounds instead (same values, same order).
 // Supported: N % 32 == 0, 32 <= N <= 512, m <= 32; other shapes use the CUDA-
 // core kernel (init.cu).
 #include <cstdint>
@@ -107,6 +109,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+// tcgen05.ld without the wait: the registers are valid only after tmem_wait()
+// + tmem_regs_ready() (the empty asm ties every later use of r to a point after
+// the wait, so the compiler cannot hoist a consumer above it)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_regs_ready(uint32_t (&r)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; i++) asm volatile("" : "+r"(r[i]));
 }
 
 // bits of chunk [c0, c0 + 32) inside the linear interval [lo, hi] (lo <= hi)
@@ -284,7 +305,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     // ---- epilogue: (pixel = TMEM lane) x (column split) per thread ----
-    load_tile(tile + gridDim.x);  // next tile's z in flight during the epilogue
+    // the next tile's z in flight during the epilogue (init_depths: after the
+    // TMEM scan, whose two 32-register chunk buffers would otherwise push the
+    // prefetched rows into local memory)
+    if (!PICK) load_tile(tile + gridDim.x);
     const long long pix = row0 + prow;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     float v[32];
@@ -312,84 +336,147 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
       }
     } else {
       uint32_t* cand = cand_all + prow;  // cand[c * TC_M]
-      // round 0 over this split's chunks: candidate masks and the local best
-      float best = 0.f;
-      int bn = -1;
+      // Round 0 over this split's chunks: the candidate masks, and the
+      // candidates' values in increasing n appended to a per-thread list in
+      // the A buffers (free until the next tile; entry e of thread tid at
+      // lst[e * TC_THREADS]: lanes with different counts still hit distinct
+      // banks).  The pick rounds then walk the list instead of re-reading and
+      // arg-maxing every TMEM column (a grid of a degree-m trigonometric sum
+      // has few local maxima).  33 consecutive grid points hold at most 17
+      // candidates (no two are adjacent: g_n >= g_{n+1} and g_{n+1} > g_n
+      // exclude each other), so a chunk starting with <= CAP - 17 entries
+      // always fits; otherwise the thread is marked overflowed and its rounds
+      // take the TMEM path below (same values, same tie order).
+      constexpr int CAP = (int)(4 * A_CHUNK / 4) / TC_THREADS;  // 32 entries
+      float* const lst = reinterpret_cast<float*>(a_hi) + tid;
+      float* wp = lst;
+      int step = TC_THREADS;
+      bool ovf = false;
       if (c1 > c0) {
-        tmem_ld32(trow + (uint32_t)(((c0 + NC - 1) % NC) * 32), v);
-        float prevv = v[31];  // g[32 c0 - 1] (circular)
-        tmem_ld32(trow + (uint32_t)((c1 % NC) * 32), v);
-        const float nextv = v[0];  // g[32 c1] (circular)
+        uint32_t ra[32], rb[32];
+        tmem_ld32_async(trow + (uint32_t)(((c0 + NC - 1) % NC) * 32), ra);
+        tmem_ld32_async(trow + (uint32_t)((c1 % NC) * 32), rb);
+        tmem_wait();
+        tmem_regs_ready(ra);
+        tmem_regs_ready(rb);
+        float prevv = __uint_as_float(ra[31]);  // g[32 c0 - 1] (circular)
+        const float nextv = __uint_as_float(rb[0]);  // g[32 c1] (circular)
         float pend = 0.f, pendp = 0.f;
-        for (int c = c0; c < c1; c++) {
-          tmem_ld32(trow + (uint32_t)(c * 32), v);
+        tmem_ld32_async(trow + (uint32_t)(c0 * 32), ra);
+        tmem_wait();
+        tmem_regs_ready(ra);
+        auto chunk = [&](const uint32_t(&r)[32], int c) {
+          if (wp - lst > (CAP - 17) * TC_THREADS) {
+            ovf = true;
+            step = 0;
+            wp = lst;
+          }
+          const float v0 = __uint_as_float(r[0]);
           if (c > c0) {  // element 31 of chunk c-1 (its right neighbour is v[0])
-            const bool ok = pend > 0.f && pend > pendp && pend >= v[0];
-            if (ok) cand[(c - 1) * TC_M] |= 1u << 31;
-            if (ok && pend > best) {
-              best = pend;
-              bn = (c - 1) * 32 + 31;
+            const bool ok = pend > 0.f && pend > pendp && pend >= v0;
+            if (ok) {
+              cand[(c - 1) * TC_M] |= 1u << 31;
+              *wp = pend;
+              wp += step;
             }
           }
           uint32_t bits = 0u;
-          float x[32];
 #pragma unroll
           for (int i = 0; i < 31; i++) {
-            const float g = v[i], gp = i == 0 ? prevv : v[i - 1];
-            const bool ok = g > 0.f && g > gp && g >= v[i + 1];
-            bits |= ok ? (1u << i) : 0u;
-            x[i] = ok ? g : 0.f;  // candidates are > 0
-          }
-          x[31] = 0.f;
-          float cm;
-          int ci;
-          tree_argmax32(x, cm, ci);
-          if (cm > best) {
-            best = cm;
-            bn = c * 32 + ci;
+            const float g = __uint_as_float(r[i]), gp = i == 0 ? prevv : __uint_as_float(r[i - 1]);
+            const bool ok = g > 0.f && g > gp && g >= __uint_as_float(r[i + 1]);
+            if (ok) {
+              bits |= 1u << i;
+              *wp = g;
+              wp += step;
+            }
           }
           cand[c * TC_M] = bits;
-          pend = v[31];
-          pendp = v[30];
-          prevv = v[31];
+          pend = __uint_as_float(r[31]);
+          pendp = __uint_as_float(r[30]);
+          prevv = pend;
+        };
+        for (int c = c0; c < c1; c += 2) {  // chunk c in ra; chunk c + 1 loads while c is scanned
+          if (c + 1 < c1) tmem_ld32_async(trow + (uint32_t)((c + 1) * 32), rb);
+          chunk(ra, c);
+          if (c + 1 >= c1) break;
+          tmem_wait();
+          tmem_regs_ready(rb);
+          if (c + 2 < c1) tmem_ld32_async(trow + (uint32_t)((c + 2) * 32), ra);
+          chunk(rb, c + 1);
+          if (c + 2 < c1) {
+            tmem_wait();
+            tmem_regs_ready(ra);
+          }
         }
         const bool ok = pend > 0.f && pend > pendp && pend >= nextv;  // n = 32 c1 - 1
-        if (ok) cand[(c1 - 1) * TC_M] |= 1u << 31;
-        if (ok && pend > best) {
-          best = pend;
-          bn = c1 * 32 - 1;
+        if (ok) {
+          cand[(c1 - 1) * TC_M] |= 1u << 31;
+          *wp = pend;
         }
       }
-      // K rounds: combine the splits' local bests (largest g, then smallest n);
-      // every split thread of a pixel keeps the same pick list
+      load_tile(tile + gridDim.x);
+      const bool wovf = __any_sync(0xffffffffu, ovf);
+      // per-chunk eligibility masks in registers (a split holds <= NC / 4 <= 4
+      // chunks), narrowed by the newest pick's exclusion zone each round
+      constexpr int MAXC = 16 / TC_SPLIT;
+      uint32_t cbm[MAXC], el[MAXC];
+      int pos0[MAXC];
+      {
+        int pp = 0;
+#pragma unroll
+        for (int i = 0; i < MAXC; i++) {
+          cbm[i] = c0 + i < c1 ? cand[(c0 + i) * TC_M] : 0u;
+          el[i] = cbm[i];
+          pos0[i] = pp;
+          pp += __popc(cbm[i]);
+        }
+      }
+      // K rounds: each split's best outside the exclusion zones of the picks so
+      // far, combined across the splits (largest g, then smallest n); every
+      // split thread of a pixel keeps the same pick list
       int pick[KK];
       float pg[KK];
-      int cnt = 0;
+      int cnt = 0, lastp = 0;
       for (uint32_t k = 0; k < a.K; k++) {
         const int buf = k & 1;
-        if (k > 0) {  // local best outside the exclusion zones of the picks so far
-          best = 0.f;
-          bn = -1;
-          const bool live = cnt == (int)k;
-          for (int c = c0; c < c1; c++) {
-            uint32_t elig = 0u;
-            if (live) {
-              elig = cand[c * TC_M];
+        float best = 0.f;
+        int bn = -1;
+        const bool live = cnt == (int)k;
+        if (k > 0 && live) {
 #pragma unroll
-              for (int q = 0; q < KK; q++)
-                if (q < cnt) elig &= ~excl_bits(pick[q], D, N, c * 32);
+          for (int i = 0; i < MAXC; i++) el[i] &= ~excl_bits(lastp, D, N, (c0 + i) * 32);
+        }
+        if (live && !ovf) {
+#pragma unroll
+          for (int i = 0; i < MAXC; i++) {
+            uint32_t e = el[i];
+            while (e) {  // increasing n: strict > keeps the smaller n
+              const int j = __ffs(e) - 1;
+              e &= e - 1u;
+              const float val = lst[(pos0[i] + __popc(cbm[i] & ((1u << j) - 1u))) * TC_THREADS];
+              if (val > best) {
+                best = val;
+                bn = (c0 + i) * 32 + j;
+              }
             }
-            if (!__any_sync(0xffffffffu, elig != 0u)) continue;
-            tmem_ld32(trow + (uint32_t)(c * 32), v);
-            float x[32];
+          }
+        }
+        if (wovf) {  // warp-uniform: TMEM re-reads for the overflowed lanes
 #pragma unroll
-            for (int i = 0; i < 32; i++) x[i] = ((elig >> i) & 1u) ? v[i] : 0.f;
+          for (int i = 0; i < MAXC; i++) {
+            if (c0 + i >= c1) break;
+            const uint32_t elig = live && ovf ? el[i] : 0u;
+            if (!__any_sync(0xffffffffu, elig != 0u)) continue;
+            tmem_ld32(trow + (uint32_t)((c0 + i) * 32), v);
+#pragma unroll
+            for (int q = 0; q < 32; q++) v[q] = ((elig >> q) & 1u) ? v[q] : 0.f;
             float cm;
             int ci;
-            tree_argmax32(x, cm, ci);
+            tree_argmax32(v, cm, ci);
             if (cm > best) {
               best = cm;
-              bn = c * 32 + ci;
+              bn = (c0 + i) * 32 + ci;
             }
           }
         }
@@ -414,6 +501,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
               pick[q] = gi;
               pg[q] = gb;
             }
+          lastp = gi;
           cnt++;
         }
       }
