@@ -40,6 +40,7 @@
 // Supported: N % 32 == 0, 32 <= N <= 512, m <= 32; other shapes use the CUDA-
 // core kernel (init.cu).
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -52,6 +53,7 @@ constexpr int TC_M = 128;          // pixels per tile (TMEM lanes)
 constexpr int TC_SPLIT = 4;        // column splits of the epilogue: 4 warps per TMEM lane quarter
 constexpr int TC_THREADS = TC_M * TC_SPLIT;
 constexpr uint32_t A_CHUNK = TC_M * 128;  // one 128-byte swizzle column of A: 16 KB
+constexpr int PICK_CAP = 12;              // candidate-list entries per thread (init_depths): 24 KB
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -184,7 +186,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
   unsigned char* a_lo = a_hi + 2 * A_CHUNK;
   unsigned char* b_hi = a_lo + 2 * A_CHUNK;          // 2 K columns x NH rows x 128 B
   unsigned char* b_lo = b_hi + 2 * NH * 128;
-  uint32_t* cand_all = reinterpret_cast<uint32_t*>(b_lo + 2 * NH * 128);  // [NC][TC_M] (PICK)
   __shared__ __align__(8) uint64_t mma_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ float xb_v[2][TC_SPLIT][TC_M];  // per-round local bests of the column splits
@@ -257,62 +258,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
   };
   load_tile(blockIdx.x);
 
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long row0 = tile * TC_M;
-    // ---- A: z rows -> [even l | odd l] K columns, split hi / lo, swizzled ----
-    {
-      const uint32_t i = (uint32_t)lane >> 1, col = (lane & 1) ? 0u : 1u;  // frequency l = lane + 1
+  // ---- A staging and the MMAs of one tile (shared by both epilogues) ----
+  // z rows (zpre) -> [even l | odd l] K columns, split hi / lo, swizzled
+  auto stage_a = [&]() {
+    const uint32_t i = (uint32_t)lane >> 1, col = (lane & 1) ? 0u : 1u;  // frequency l = lane + 1
 #pragma unroll
-      for (int rr = 0; rr < RPW; rr++) {
-        const uint32_t r = (uint32_t)(warp * RPW + rr);
-        const float2 v = zpre[rr];
-        const float hx = __uint_as_float(tf32_rna(v.x)), hy = __uint_as_float(tf32_rna(v.y));
-        const float lx = __uint_as_float(tf32_rna(v.x - hx)), ly = __uint_as_float(tf32_rna(v.y - hy));
-        const uint32_t off = col * A_CHUNK + sw_off(r, i);
-        *reinterpret_cast<float2*>(a_hi + off) = make_float2(hx, hy);
-        *reinterpret_cast<float2*>(a_lo + off) = make_float2(lx, ly);
-      }
+    for (int rr = 0; rr < RPW; rr++) {
+      const uint32_t r = (uint32_t)(warp * RPW + rr);
+      const float2 v = zpre[rr];
+      const float hx = __uint_as_float(tf32_rna(v.x)), hy = __uint_as_float(tf32_rna(v.y));
+      const float lx = __uint_as_float(tf32_rna(v.x - hx)), ly = __uint_as_float(tf32_rna(v.y - hy));
+      const uint32_t off = col * A_CHUNK + sw_off(r, i);
+      *reinterpret_cast<float2*>(a_hi + off) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(a_lo + off) = make_float2(lx, ly);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  };
+  // one thread, after a CTA barrier that follows stage_a and the last TMEM reads
+  auto issue_mma = [&]() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const uint32_t dt = tmem + (uint32_t)(h * NH);
-        int first = 1;
+    for (int h = 0; h < 2; h++) {
+      const uint32_t dt = tmem + (uint32_t)(h * NH);
+      int first = 1;
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
-          const uint32_t id = (h == 1 && c == 1) ? idesc_neg : idesc;
+      for (int c = 0; c < 2; c++) {
+        const uint32_t id = (h == 1 && c == 1) ? idesc_neg : idesc;
 #pragma unroll
-          for (int kk = 0; kk < 4; kk++) {
-            const uint32_t ao = (uint32_t)c * A_CHUNK + (uint32_t)kk * 32u;
-            const uint32_t bo = (uint32_t)c * (uint32_t)NH * 128u + (uint32_t)kk * 32u;
-            mma_tf32(dt, sw128_desc(sa_hi + ao), sw128_desc(sb_hi + bo), id, first ? 0u : 1u);
-            mma_tf32(dt, sw128_desc(sa_hi + ao), sw128_desc(sb_lo + bo), id, 1u);
-            mma_tf32(dt, sw128_desc(sa_lo + ao), sw128_desc(sb_hi + bo), id, 1u);
-            first = 0;
-          }
+        for (int kk = 0; kk < 4; kk++) {
+          const uint32_t ao = (uint32_t)c * A_CHUNK + (uint32_t)kk * 32u;
+          const uint32_t bo = (uint32_t)c * (uint32_t)NH * 128u + (uint32_t)kk * 32u;
+          mma_tf32(dt, sw128_desc(sa_hi + ao), sw128_desc(sb_hi + bo), id, first ? 0u : 1u);
+          mma_tf32(dt, sw128_desc(sa_hi + ao), sw128_desc(sb_lo + bo), id, 1u);
+          mma_tf32(dt, sw128_desc(sa_lo + ao), sw128_desc(sb_hi + bo), id, 1u);
+          first = 0;
         }
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       su32(&mma_bar))
-                   : "memory");
     }
-    mbar_wait_parity(&mma_bar, phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     su32(&mma_bar))
+                 : "memory");
+  };
+  const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+  float v[32];
 
-    // ---- epilogue: (pixel = TMEM lane) x (column split) per thread ----
-    // the next tile's z in flight during the epilogue (init_depths: after the
-    // TMEM scan, whose two 32-register chunk buffers would otherwise push the
-    // prefetched rows into local memory)
-    if (!PICK) load_tile(tile + gridDim.x);
-    const long long pix = row0 + prow;
-    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    float v[32];
-    if (!PICK) {
+  if constexpr (!PICK) {
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const long long row0 = tile * TC_M;
+      stage_a();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) issue_mma();
+      mbar_wait_parity(&mma_bar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      load_tile(tile + gridDim.x);  // the next tile's z in flight during the epilogue
       // per 32-column chunk: the warp's 32 rows through shared memory (the A
       // buffers are free until the next tile; float4 slots XOR-swizzled) so
       // each warp store covers whole 128-byte row runs
@@ -334,24 +334,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
         }
         __syncwarp();
       }
-    } else {
-      uint32_t* cand = cand_all + prow;  // cand[c * TC_M]
-      // Round 0 over this split's chunks: the candidate masks, and the
-      // candidates' values in increasing n appended to a per-thread list in
-      // the A buffers (free until the next tile; entry e of thread tid at
-      // lst[e * TC_THREADS]: lanes with different counts still hit distinct
-      // banks).  The pick rounds then walk the list instead of re-reading and
-      // arg-maxing every TMEM column (a grid of a degree-m trigonometric sum
-      // has few local maxima).  33 consecutive grid points hold at most 17
-      // candidates (no two are adjacent: g_n >= g_{n+1} and g_{n+1} > g_n
-      // exclude each other), so a chunk starting with <= CAP - 17 entries
-      // always fits; otherwise the thread is marked overflowed and its rounds
-      // take the TMEM path below (same values, same tie order).
-      constexpr int CAP = (int)(4 * A_CHUNK / 4) / TC_THREADS;  // 32 entries
-      float* const lst = reinterpret_cast<float*>(a_hi) + tid;
+      // the next tile's MMAs overwrite the accumulator and A: all reads done first
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+    }
+  } else {
+    // init_depths, pipelined across tiles: tile t+1's z loads overlap tile t's
+    // MMAs; A(t+1) is staged as soon as MMA(t) has completed; the TMEM scan of
+    // tile t leaves every candidate in shared memory (masks in registers,
+    // values in the list), so MMA(t+1) is issued right after the scan and runs
+    // under tile t's pick rounds (unless some thread's list overflowed: then
+    // the rounds re-read TMEM and MMA(t+1) waits for them).
+    constexpr int MAXC = 16 / TC_SPLIT;  // chunks per split (N <= 512)
+    float* const lst = reinterpret_cast<float*>(b_lo + 2 * NH * 128) + tid;  // entry e at lst[e * TC_THREADS]
+    float* const lend = lst + a.list_cap * TC_THREADS;
+    long long tile = blockIdx.x;
+    if (tile < ntiles) {
+      stage_a();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) issue_mma();
+    }
+    for (; tile < ntiles; tile += gridDim.x) {
+      const long long row0 = tile * TC_M, nxt = tile + gridDim.x;
+      const bool has_next = nxt < ntiles;
+      load_tile(nxt);
+      mbar_wait_parity(&mma_bar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (has_next) stage_a();  // MMA(t) has read A
+      const long long pix = row0 + prow;
+
+      // ---- TMEM scan: candidate masks (registers) and values (list) ----
+      // candidate: g_n > 0, g_n > g_{n-1}, g_n >= g_{n+1} (circular); values
+      // appended in increasing n while the list has room; a thread with more
+      // than PICK_CAP candidates (measured at C5: at most 9 of 128 columns) is
+      // marked overflowed
+      uint32_t cbm[MAXC];
+#pragma unroll
+      for (int i = 0; i < MAXC; i++) cbm[i] = 0u;
       float* wp = lst;
-      int step = TC_THREADS;
-      bool ovf = false;
       if (c1 > c0) {
         uint32_t ra[32], rb[32];
         tmem_ld32_async(trow + (uint32_t)(((c0 + NC - 1) % NC) * 32), ra);
@@ -359,82 +381,76 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
         tmem_wait();
         tmem_regs_ready(ra);
         tmem_regs_ready(rb);
-        float prevv = __uint_as_float(ra[31]);  // g[32 c0 - 1] (circular)
+        float prevv = __uint_as_float(ra[31]);       // g[32 c0 - 1] (circular)
         const float nextv = __uint_as_float(rb[0]);  // g[32 c1] (circular)
         float pend = 0.f, pendp = 0.f;
         tmem_ld32_async(trow + (uint32_t)(c0 * 32), ra);
         tmem_wait();
         tmem_regs_ready(ra);
-        auto chunk = [&](const uint32_t(&r)[32], int c) {
-          if (wp - lst > (CAP - 17) * TC_THREADS) {
-            ovf = true;
-            step = 0;
-            wp = lst;
-          }
+        auto chunk = [&](uint32_t(&r)[32], uint32_t(&rn)[32], int i) {
+          const int c = c0 + i;
+          if (c + 1 < c1) tmem_ld32_async(trow + (uint32_t)((c + 1) * 32), rn);  // in flight during the scan
           const float v0 = __uint_as_float(r[0]);
-          if (c > c0) {  // element 31 of chunk c-1 (its right neighbour is v[0])
+          if (i > 0) {  // element 31 of chunk c-1 (its right neighbour is v[0])
             const bool ok = pend > 0.f && pend > pendp && pend >= v0;
-            if (ok) {
-              cand[(c - 1) * TC_M] |= 1u << 31;
+            if (ok) cbm[i - 1] |= 1u << 31;
+            if (ok && wp < lend) {
               *wp = pend;
-              wp += step;
+              wp += TC_THREADS;
             }
           }
           uint32_t bits = 0u;
 #pragma unroll
-          for (int i = 0; i < 31; i++) {
-            const float g = __uint_as_float(r[i]), gp = i == 0 ? prevv : __uint_as_float(r[i - 1]);
-            const bool ok = g > 0.f && g > gp && g >= __uint_as_float(r[i + 1]);
-            if (ok) {
-              bits |= 1u << i;
+          for (int e = 0; e < 31; e++) {
+            const float g = __uint_as_float(r[e]), gp = e == 0 ? prevv : __uint_as_float(r[e - 1]);
+            const bool ok = g > 0.f && g > gp && g >= __uint_as_float(r[e + 1]);
+            if (ok) bits |= 1u << e;
+            if (ok && wp < lend) {
               *wp = g;
-              wp += step;
+              wp += TC_THREADS;
             }
           }
-          cand[c * TC_M] = bits;
+          cbm[i] = bits;
           pend = __uint_as_float(r[31]);
           pendp = __uint_as_float(r[30]);
           prevv = pend;
-        };
-        for (int c = c0; c < c1; c += 2) {  // chunk c in ra; chunk c + 1 loads while c is scanned
-          if (c + 1 < c1) tmem_ld32_async(trow + (uint32_t)((c + 1) * 32), rb);
-          chunk(ra, c);
-          if (c + 1 >= c1) break;
-          tmem_wait();
-          tmem_regs_ready(rb);
-          if (c + 2 < c1) tmem_ld32_async(trow + (uint32_t)((c + 2) * 32), ra);
-          chunk(rb, c + 1);
-          if (c + 2 < c1) {
+          if (c + 1 < c1) {
             tmem_wait();
-            tmem_regs_ready(ra);
+            tmem_regs_ready(rn);
           }
-        }
-        const bool ok = pend > 0.f && pend > pendp && pend >= nextv;  // n = 32 c1 - 1
-        if (ok) {
-          cand[(c1 - 1) * TC_M] |= 1u << 31;
-          *wp = pend;
-        }
-      }
-      load_tile(tile + gridDim.x);
-      const bool wovf = __any_sync(0xffffffffu, ovf);
-      // per-chunk eligibility masks in registers (a split holds <= NC / 4 <= 4
-      // chunks), narrowed by the newest pick's exclusion zone each round
-      constexpr int MAXC = 16 / TC_SPLIT;
-      uint32_t cbm[MAXC], el[MAXC];
-      int pos0[MAXC];
-      {
-        int pp = 0;
+        };
 #pragma unroll
         for (int i = 0; i < MAXC; i++) {
-          cbm[i] = c0 + i < c1 ? cand[(c0 + i) * TC_M] : 0u;
-          el[i] = cbm[i];
-          pos0[i] = pp;
-          pp += __popc(cbm[i]);
+          if (c0 + i >= c1) break;
+          if (i & 1)
+            chunk(rb, ra, i);
+          else
+            chunk(ra, rb, i);
         }
+        const bool ok = pend > 0.f && pend > pendp && pend >= nextv;  // n = 32 c1 - 1
+#pragma unroll
+        for (int i = 0; i < MAXC; i++)
+          if (ok && i == c1 - c0 - 1) cbm[i] |= 1u << 31;
+        if (ok && wp < lend) *wp = pend;
       }
-      // K rounds: each split's best outside the exclusion zones of the picks so
-      // far, combined across the splits (largest g, then smallest n); every
-      // split thread of a pixel keeps the same pick list
+      int ncand = 0, pos0[MAXC];
+#pragma unroll
+      for (int i = 0; i < MAXC; i++) {
+        pos0[i] = ncand;
+        ncand += __popc(cbm[i]);
+      }
+      const bool ovf = ncand > a.list_cap;
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      const bool any_ovf = __syncthreads_or(ovf) != 0;  // also: A(t+1) staged by every warp
+      if (has_next && !any_ovf && tid == 0) issue_mma();  // runs under the pick rounds
+      const bool wovf = __any_sync(0xffffffffu, ovf);
+
+      // ---- K rounds: each split's best outside the exclusion zones of the
+      // picks so far, combined across the splits (largest g, then smallest n);
+      // every split thread of a pixel keeps the same pick list ----
+      uint32_t el[MAXC];
+#pragma unroll
+      for (int i = 0; i < MAXC; i++) el[i] = cbm[i];
       int pick[KK];
       float pg[KK];
       int cnt = 0, lastp = 0;
@@ -443,7 +459,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
         float best = 0.f;
         int bn = -1;
         const bool live = cnt == (int)k;
-        if (k > 0 && live) {
+        if (k > 0 && live) {  // narrowed by the newest pick's exclusion zone
 #pragma unroll
           for (int i = 0; i < MAXC; i++) el[i] &= ~excl_bits(lastp, D, N, (c0 + i) * 32);
         }
@@ -462,7 +478,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
             }
           }
         }
-        if (wovf) {  // warp-uniform: TMEM re-reads for the overflowed lanes
+        if (wovf) {  // warp-uniform: TMEM re-reads for the overflowed lanes (MMA(t+1) not issued yet)
 #pragma unroll
           for (int i = 0; i < MAXC; i++) {
             if (c0 + i >= c1) break;
@@ -505,8 +521,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
           cnt++;
         }
       }
-      if (split == 0 && pix < a.npix) {
-        // sort by depth (insertion sort on the register arrays: compile-time indices)
+      if (pix < a.npix) {
+        // sort by depth (insertion sort on the register arrays: compile-time
+        // indices); the four split threads of a pixel write every 4th pick
 #pragma unroll
         for (int x = 1; x < KK; x++)
 #pragma unroll
@@ -519,27 +536,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
               pg[y] = pg[y - 1];
               pg[y - 1] = tg;
             }
-        const double tfirst = cnt ? (double)pick[0] * (double)a.T / (double)N : 0.0;
 #pragma unroll
         for (int k = 0; k < KK; k++) {
           if (k >= (int)a.K) break;
+          if ((k & (TC_SPLIT - 1)) != split) continue;
           const size_t o = (size_t)pix * a.K + k;
           if (k < cnt) {
             a.t_out[o] = (float)((double)pick[k] * (double)a.T / (double)N);
             a.g_out[o] = pg[k];
             a.a_out[o] = fminf(fmaxf(pg[k] * a.inv_sh2, 0.f), 1.f);
           } else {
+            const double tfirst = cnt ? (double)pick[0] * (double)a.T / (double)N : 0.0;
             a.t_out[o] = (float)fmod(tfirst + 0.5 * (double)a.T, (double)a.T);
             a.g_out[o] = 0.f;
             a.a_out[o] = 0.f;
           }
         }
-        a.count[pix] = cnt;
+        if (split == TC_SPLIT - 1) a.count[pix] = cnt;
       }
+      if (has_next && any_ovf) {  // the rounds' TMEM reads are done
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) issue_mma();
+      }
+      __syncthreads();  // the next scan rewrites the lists and the combine buffers
     }
-    // the next tile's MMAs overwrite the accumulator: all TMEM reads done first
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
   }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
@@ -547,7 +568,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
 
 size_t bp_tc_smem(uint32_t N, bool pick) {
   const size_t nh = N / 2;
-  return 1024 + 4 * (size_t)A_CHUNK + 2 * 2 * nh * 128 + (pick ? sizeof(uint32_t) * (N / 32) * TC_M : 0);
+  return 1024 + 4 * (size_t)A_CHUNK + 2 * 2 * nh * 128 + (pick ? sizeof(float) * PICK_CAP * TC_THREADS : 0);
 }
 
 }  // namespace
@@ -564,10 +585,15 @@ cudaError_t launch_backproject_tc(const BpArgs& a, bool pick, cudaStream_t s, in
   static SmemAttrOnce attr[6];
   cudaError_t e = smem_attr_once(attr[vi], fn, (int)bp_tc_smem(512, pick));
   if (e != cudaSuccess) return e;
+  // SRT3D_INIT_LIST_CAP (tests only) shrinks the candidate list so that the
+  // overflow path (TMEM re-reads, MMA of the next tile after the rounds) runs
+  BpArgs b = a;
+  b.list_cap = PICK_CAP;
+  if (const char* e = getenv("SRT3D_INIT_LIST_CAP")) b.list_cap = max(0, min(PICK_CAP, atoi(e)));
   const long long tiles = (a.npix + TC_M - 1) / TC_M;
   long long grid = num_sms;  // one persistent CTA per SM (the accumulator holds up to all 512 TMEM columns)
   if (grid > tiles) grid = tiles;
-  fn<<<(unsigned)grid, TC_THREADS, bp_tc_smem(a.N, pick), s>>>(a);
+  fn<<<(unsigned)grid, TC_THREADS, bp_tc_smem(a.N, pick), s>>>(b);
   return cudaGetLastError();
 }
 

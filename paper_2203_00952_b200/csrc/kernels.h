@@ -210,6 +210,7 @@ struct BpArgs {
   uint32_t T, m, N, K, min_sep;
   float inv_sh2;    // 1 / sum_l hhat_l^2
   float hh[MAX_M];  // hhat_l
+  int list_cap;     // tensor-core init_depths: candidate-list entries per thread (set by its launcher)
 };
 cudaError_t launch_backproject(const BpArgs& a, bool pick, cudaStream_t s, int num_sms);
 // tensor-core backprojection (init_tc.cu): N % 32 == 0, 32 <= N <= 512, m <= 32

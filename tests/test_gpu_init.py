@@ -172,6 +172,37 @@ def test_init_depths_parity(gpu, oracle_mod, inputs_mod, T, m, N, K, min_sep, si
         assert np.all((ag >= 0) & (ag <= 1)) and np.all(cg <= K)
 
 
+@pytest.mark.parametrize("cap", ["0", "2", "5"])
+def test_init_depths_tc_list_overflow(gpu, oracle_mod, inputs_mod, monkeypatch, cap):
+    """Tensor-core init_depths keeps each thread's candidates in a shared-memory list
+    (DESIGN.md §5.5); a thread with more candidates than the list holds re-reads TMEM in
+    its pick rounds and the next tile's MMAs wait for them.  Shrinking the list
+    (SRT3D_INIT_LIST_CAP, read per launch) sends all (0) or some (2, 5) threads down that
+    path over several tiles per CTA: the picks must be bitwise those of the default list,
+    and match the oracle (near-ties as in _check_picks)."""
+    import torch
+
+    T, m, N, K, min_sep, sigma = 8192, 32, 512, 4, 40, 6.0
+    npix = 148 * 128 + 300
+    bins, offs = inputs_mod.random_csr(npix=npix, T=T, max_n=300, seed=77)
+    z = _gpu_sketch(gpu, bins, offs, T, m)
+    ref = [x.cpu().numpy() for x in gpu.srt3d_init_depths(z, sigma, T, N, K, min_sep)]
+    monkeypatch.setenv("SRT3D_INIT_LIST_CAP", cap)
+    out = [x.cpu().numpy() for x in gpu.srt3d_init_depths(z, sigma, T, N, K, min_sep)]
+    torch.cuda.synchronize()
+    for r, o in zip(ref, out):
+        assert np.array_equal(r.view(np.uint32) if r.dtype == np.float32 else r,
+                              o.view(np.uint32) if o.dtype == np.float32 else o)
+    idx = np.random.default_rng(1).choice(npix, 300, replace=False)
+    zh = z.cpu().numpy()[idx]
+    gfull = oracle_mod.backproject(zh, sigma, T, N)
+    to, go, ao, co = oracle_mod.init_depths(gfull, sigma, T, m, K, min_sep)
+    S = np.sum(_hh(sigma, T, m) * np.abs(zh), axis=1)
+    bad = _check_picks(out[0][idx], out[3][idx], 2e-5 * S, to.astype(np.float32), co, lambda i: gfull[i], T, N,
+                       min_sep)
+    assert bad <= 15, bad
+
+
 def test_init_depths_edge_cases(gpu, oracle_mod):
     """Flat zero sketch -> no picks (A14 fill); K larger than the peaks; invalid args write nothing."""
     import torch
