@@ -498,7 +498,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(const BpArgs a) {
         }
         xb_v[buf][split][prow] = best;
         xb_i[buf][split][prow] = bn;
-        __syncthreads();
+        // a pixel's four split threads sit in the four warps of its TMEM lane
+        // quarter: a named barrier over those 128 threads (not the CTA) joins them
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(4 * 32) : "memory");
         float gb = 0.f;
         int gi = -1;
 #pragma unroll
