@@ -705,8 +705,9 @@ def run_srt3d(args):
                       "peak": tf32_peak / 1e12, "unit": "TFLOP/s", "frac": t_alg / tf32_peak / t_run,
                       "peak_source": "MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (TF32 dense)",
                       "alg_flops_per_launch": t_alg, "executed_tensor_flops_per_launch": 3.0 * f.npix * 2.0 * 64 * n_grid,
-                      "note": "tcgen05 kind::tf32 (3-term split) + pick epilogue; the epilogue (candidate scan and K "
-                              "rounds over the TMEM accumulator) bounds the kernel, the MMAs are ~14% of it (ncu)"}
+                      "note": "tcgen05 kind::tf32 (3-term split) + pick epilogue; the next tile's MMAs run under "
+                              "the current tile's pick rounds, and the TMEM candidate scan (~6 instructions per grid "
+                              "point) bounds the kernel (profiles/r02_ncu_init_C5.json, DESIGN.md 5.5)"}
         else:
             d_roof = roofline("srt3d_init_depths", d_b, d_f, init_ms["depths_ms"])
         init = {"init_depths": {"kernel": "srt3d_init_depths", "grid_N": init_ms["N"], "K": init_ms["K"],
