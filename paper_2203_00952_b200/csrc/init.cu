@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace srt3d {
 
@@ -246,8 +247,107 @@ __global__ void __launch_bounds__(BP_WARPS * 32) init_k1_kernel(const BpArgs a) 
   a.a_out[pix] = al;
 }
 
+// The same closed form with the warp's z slab staged by TMA (m % 16 == 0,
+// m <= 64): one lane issues m/16 boxes of 32 rows x 32 floats (128-byte
+// swizzle: 16-byte chunk c of row r at c ^ (r & 7), conflict-free per-thread
+// row reads) on one mbarrier per box before anything else, so a warp's 8-16
+// KB are in flight from its first instruction (the cp.async kernel above
+// issues 32 8-byte copies per lane with their address arithmetic first);
+// later boxes are awaited only when the frequency loop reaches them.  Rows
+// past the frame end are zero-filled by the TMA unit.  Same arithmetic as
+// init_k1_kernel, bit for bit.
+constexpr int K1_WARPS = 4;
+template <int NBOX>
+__global__ void __launch_bounds__(K1_WARPS * 32) init_k1_tma_kernel(const BpArgs a,
+                                                                    const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ unsigned char k1t_raw[];
+  unsigned char* sm = k1t_raw + ((1024u - (smem_u32(k1t_raw) & 1023u)) & 1023u);  // 1 KB aligned (swizzle atoms)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* tile = sm + (size_t)warp * NBOX * 4096;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)K1_WARPS * NBOX * 4096) + warp * NBOX;
+  const long long row0 = ((long long)blockIdx.x * K1_WARPS + warp) * 32;
+  if (row0 >= a.npix) return;  // whole warp
+  if (lane == 0) {
+#pragma unroll
+    for (int h = 0; h < NBOX; h++) mbar_init(bar + h, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int h = 0; h < NBOX; h++) {
+      mbar_expect_tx(bar + h, 4096u);
+      tma_load_2d(tile + h * 4096, &tm, h * 32, (int)row0, bar + h);
+    }
+  }
+  __syncwarp();
+  const int m = 16 * NBOX;
+  const unsigned char* zr = tile + lane * 128;
+  const int r7 = (lane & 7) << 4;
+  auto zload = [&](int j) {  // z_j of this lane's row from box j / 16
+    const float4 z2 = *reinterpret_cast<const float4*>(zr + (j / 16) * 4096 + ((((j % 16) / 2) << 4) ^ r7));
+    return (j & 1) ? make_float2(z2.z, z2.w) : make_float2(z2.x, z2.y);
+  };
+  mbar_wait(bar, 0u);
+  const float2 z1 = zload(0);
+  float tf = 0.f, al = 0.f;
+  const bool live = hypot((double)z1.x, (double)z1.y) > 1e-12;
+  if (live) {
+    double t = (double)a.T * atan2((double)z1.y, (double)z1.x) / (2.0 * 3.14159265358979323846);
+    if (t < 0.0) t += (double)a.T;
+    tf = (float)t;
+    if (tf >= (float)a.T) tf = 0.f;  // rounded up to T: the same point of the circle
+  }
+  const uint32_t q = phase_q32(tf, 1.0 / (double)a.T);
+  const float2 w = phasor_q32(q);
+  const u64 W = pk(w.x, w.y), Wn = pk(-w.y, w.x);
+  u64 P = W;
+  float num = 0.f;
+#pragma unroll
+  for (int j = 0; j < m; j++) {
+    if (j > 0 && j % 16 == 0) mbar_wait(bar + j / 16, 0u);  // every lane: the warp stays converged
+    if (j > 0) {
+      if ((j & 31) == 0) {
+        const float2 p = phasor_q32(q * (uint32_t)(j + 1));
+        P = pk(p.x, p.y);
+      } else {
+        P = cmul2(P, W, Wn);
+      }
+    }
+    const float2 zj = zload(j);
+    num = fmaf(a.hh[j], fmaf(lo_of(P), zj.x, hi_of(P) * zj.y), num);  // hhat_j Re(conj(p_j) z_j)
+  }
+  if (live) al = fminf(fmaxf(num * a.inv_sh2, 0.f), 1.f);
+  const long long pix = row0 + lane;
+  if (pix < a.npix) {
+    a.t_out[pix] = tf;
+    a.a_out[pix] = al;
+  }
+}
+
 cudaError_t launch_init_k1(const BpArgs& a, cudaStream_t s) {
   if (a.npix <= 0) return cudaSuccess;
+  // TMA staging where the shape allows it (SRT3D_INIT_K1_CPASYNC=1 forces the cp.async kernel: A/B and parity)
+  const char* force = getenv("SRT3D_INIT_K1_CPASYNC");
+  if (!(force && force[0] == '1') && a.m % 16 == 0 && a.m <= 64 && ((uintptr_t)a.z & 15u) == 0 &&
+      a.npix < (1ll << 31)) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    CUtensorMap tm;
+    const cuuint64_t gdim[2] = {(cuuint64_t)(2 * a.m), (cuuint64_t)a.npix};
+    const cuuint64_t gstride[1] = {(cuuint64_t)(2 * a.m * sizeof(float))};
+    const cuuint32_t box[2] = {32u, 32u}, estride[2] = {1u, 1u};
+    if (enc && enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.z), gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      const int nbox = (int)a.m / 16;
+      void (*const fns[4])(const BpArgs, const CUtensorMap) = {init_k1_tma_kernel<1>, init_k1_tma_kernel<2>,
+                                                                init_k1_tma_kernel<3>, init_k1_tma_kernel<4>};
+      static SmemAttrOnce tattr[4];
+      const size_t tsmem = 1024 + (size_t)K1_WARPS * nbox * (4096 + 8);
+      cudaError_t e = smem_attr_once(tattr[nbox - 1], fns[nbox - 1], (int)tsmem);
+      if (e != cudaSuccess) return e;
+      const long long grid = (a.npix + 32 * K1_WARPS - 1) / (32 * K1_WARPS);
+      fns[nbox - 1]<<<(unsigned)grid, K1_WARPS * 32, tsmem, s>>>(a, tm);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = sizeof(float2) * BP_WARPS * 32 * (a.m | 1u);
   static SmemAttrOnce attr;
   cudaError_t e = smem_attr_once(attr, init_k1_kernel, (int)(sizeof(float2) * BP_WARPS * 32 * (MAX_M | 1)));

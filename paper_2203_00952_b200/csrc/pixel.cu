@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace srt3d {
 
@@ -90,30 +91,6 @@ __device__ __forceinline__ void warp_slab_store(const float2* tile, float2* gdst
 }
 
 // ---- TMA staging of the z slab (m % 16 == 0) ----------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)  // suspend-time hint (ns)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // The harness update (reading A13) for one (pixel, k); shared by the fused
 // step and K4 so both produce bit-identical results.
 __device__ __forceinline__ void update_one(const PixArgs& a, float tk, float ak, float gt, float ga, float& tn,
@@ -375,20 +352,6 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
     __syncwarp();  // every lane has read the tile before the next boxes overwrite it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (static cudart).
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  // a function-local static initialised once (thread-safe); the entry point is process-wide
-  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
-  }();
-  return fn;
 }
 
 // NEXT-2: `iters` fused data steps per pixel in one launch.

@@ -221,6 +221,33 @@ def test_init_depths_edge_cases(gpu, oracle_mod):
         gpu.srt3d_backproject(z, 1.0, T, 9000)
 
 
+@pytest.mark.parametrize("m", [16, 32, 48, 64])
+def test_init_k1_tma_equals_cp_async(gpu, oracle_mod, inputs_mod, monkeypatch, m):
+    """init_k1 stages z by TMA when m % 16 == 0; SRT3D_INIT_K1_CPASYNC=1
+    forces the cp.async kernel.  Both must give bitwise the same t and alpha (same arithmetic)
+    on a ragged frame with all-zero rows (the z_1 = 0 branch), and match the oracle."""
+    import torch
+
+    T, sigma, npix = 8192, 6.0, 148 * 128 + 45
+    bins, offs = inputs_mod.random_csr(npix=npix, T=T, max_n=200, seed=m)
+    z = _gpu_sketch(gpu, bins, offs, T, m)
+    z[::97] = 0.0
+    tg, ag = (x.cpu().numpy() for x in gpu.srt3d_init_k1(z, sigma, T))
+    monkeypatch.setenv("SRT3D_INIT_K1_CPASYNC", "1")
+    tc, ac = (x.cpu().numpy() for x in gpu.srt3d_init_k1(z, sigma, T))
+    torch.cuda.synchronize()
+    assert np.array_equal(tg.view(np.uint32), tc.view(np.uint32))
+    assert np.array_equal(ag.view(np.uint32), ac.view(np.uint32))
+    idx = np.random.default_rng(m).choice(npix, 400, replace=False)
+    zh = z.cpu().numpy()[idx]
+    to, ao = oracle_mod.init_k1(zh, sigma, T)
+    d = np.abs(tg[idx, 0].astype(np.float64) - to)
+    assert np.all(np.minimum(d, T - d) <= 0.5 * np.spacing(np.float32(T)) + 1e-9)
+    h = _hh(sigma, T, m)
+    Sa = np.sum(h * np.abs(zh), axis=1) / np.sum(h**2)
+    assert np.all(np.abs(ag[idx, 0] - ao) <= 1e-4 * Sa + 1e-7)
+
+
 @pytest.mark.parametrize("T,m,sigma", [(4613, 10, 5.0), (8192, 32, 6.0), (1024, 4, 2.0), (2500, 64, 0.0)])
 def test_init_k1_parity(gpu, oracle_mod, inputs_mod, T, m, sigma):
     import torch
