@@ -80,10 +80,71 @@ __global__ void __launch_bounds__(256) merge_kernel(const float2* __restrict__ z
   }
 }
 
+// Even m with 16-byte-aligned rows (C5): a warp merges blocks of 8 pixels
+// (8 m complex = 4 m float4, contiguous in all three arrays) with 16-byte loads,
+// consecutive lanes on consecutive addresses; lanes 0..7 read the block's
+// counts first, form the weights in fp64 exactly as merge_kernel does (one
+// rounding each), and hand them to the other lanes by shuffle; every load of
+// the block is issued before any arithmetic.  A block's pixels are touched by
+// this warp only, so in-place accumulation stays safe.
+constexpr int MERGE_BP = 8;             // pixels per block
+// V: float4 per lane per block (m <= 8 V)
+template <int MERGE_V>
+__global__ void __launch_bounds__(256) merge_kernel_v4(const float4* __restrict__ za, const uint32_t* na,
+                                                       const float4* __restrict__ zb, const uint32_t* nb,
+                                                       const uint32_t* offs_b, long long npix, uint32_t m, float4* zo,
+                                                       uint32_t* no) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t h = m / 2;  // float4 per row
+  const uint32_t nv = MERGE_BP * h;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * MERGE_BP; i0 < npix;
+       i0 += nw * MERGE_BP) {
+    const long long ip = i0 + lane;
+    uint32_t ca = 0u, cb = 0u;
+    if (lane < MERGE_BP && ip < npix) {
+      ca = na[ip];
+      cb = nb ? nb[ip] : offs_b[ip + 1] - offs_b[ip];
+    }
+    const long long e0 = i0 * h;
+    const long long eend = npix * (long long)h;
+    float4 x[MERGE_V], y[MERGE_V];
+#pragma unroll
+    for (int q = 0; q < MERGE_V; q++) {
+      const uint32_t e = (uint32_t)lane + 32u * q;
+      const bool ok = e < nv && e0 + e < eend;
+      x[q] = ok ? za[e0 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+      y[q] = ok ? zb[e0 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const uint64_t n = (uint64_t)ca + cb;
+    const double inv = n ? 1.0 / (double)n : 0.0;
+    const float wa_l = (float)((double)ca * inv), wb_l = (float)((double)cb * inv);
+#pragma unroll
+    for (int q = 0; q < MERGE_V; q++) {
+      const uint32_t e = (uint32_t)lane + 32u * q;
+      const int src = (int)(min(e, nv - 1u) / h);  // the element's pixel within the block
+      const float wa = __shfl_sync(0xffffffffu, wa_l, src), wb = __shfl_sync(0xffffffffu, wb_l, src);
+      if (e < nv && e0 + e < eend)
+        zo[e0 + e] = make_float4(fmaf(wa, x[q].x, wb * y[q].x), fmaf(wa, x[q].y, wb * y[q].y),
+                                 fmaf(wa, x[q].z, wb * y[q].z), fmaf(wa, x[q].w, wb * y[q].w));
+    }
+    if (lane < MERGE_BP && ip < npix) no[ip] = ca + cb;
+  }
+}
+
 cudaError_t launch_merge(const float* za, const uint32_t* na, const float* zb, const uint32_t* nb,
                          const uint32_t* offs_b, long long npix, uint32_t m, float* zo, uint32_t* no, cudaStream_t s,
                          int num_sms) {
   if (npix <= 0) return cudaSuccess;
+  const bool v4 = m % 2 == 0 && m <= MAX_M && (((uintptr_t)za | (uintptr_t)zb | (uintptr_t)zo) & 15u) == 0;
+  if (v4) {
+    long long grid = (npix + 8 * MERGE_BP - 1) / (8 * MERGE_BP);
+    if (grid > (long long)num_sms * 8) grid = (long long)num_sms * 8;
+    auto fn = m <= 32 ? merge_kernel_v4<4> : merge_kernel_v4<MAX_M / 8>;
+    fn<<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const float4*>(za), na, reinterpret_cast<const float4*>(zb),
+                                      nb, offs_b, npix, m, reinterpret_cast<float4*>(zo), no);
+    return cudaGetLastError();
+  }
   long long grid = (npix + 8 * MERGE_U - 1) / (8 * MERGE_U);
   if (grid > (long long)num_sms * 8) grid = (long long)num_sms * 8;
   merge_kernel<<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const float2*>(za), na,
