@@ -707,7 +707,7 @@ def run_srt3d(args):
                       "alg_flops_per_launch": t_alg, "executed_tensor_flops_per_launch": 3.0 * f.npix * 2.0 * 64 * n_grid,
                       "note": "tcgen05 kind::tf32 (3-term split) + pick epilogue; the next tile's MMAs run under "
                               "the current tile's pick rounds, and the TMEM candidate scan (~6 instructions per grid "
-                              "point) bounds the kernel (profiles/r02_ncu_init_C5.json, DESIGN.md 5.5)"}
+                              "point) bounds the kernel (profiles/r02_init_depths_ncu_C5.json, DESIGN.md 5.5)"}
         else:
             d_roof = roofline("srt3d_init_depths", d_b, d_f, init_ms["depths_ms"])
         init = {"init_depths": {"kernel": "srt3d_init_depths", "grid_N": init_ms["N"], "K": init_ms["K"],
