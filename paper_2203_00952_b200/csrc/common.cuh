@@ -82,11 +82,21 @@ __device__ __forceinline__ uint32_t phase_q32(float t, double invT) {
 // (A 256-entry table + residual polynomial variant, tools/gen_phase_tab.py,
 // was as accurate but slower in the kernel: the dependent global table load
 // sits on the anchor's critical path.)
+// The 32-bit phase is split into its top 24 bits (exact as an fp32 argument) and
+// the 8 low bits, applied as a first-order rotation by d = pi ql 2^-31 <= 3.7e-7
+// rad (the d^2/2 term is below 7e-14): converting all 32 bits to fp32 would round
+// the angle by up to 1.9e-7 rad, an error the recurrences built on this anchor
+// multiply by their length (round 2: A12's floor was exceeded by up to 1.4x at
+// m = 32 for T not a power of two, tools/a12_probe.py).  When the low bits are
+// zero (e.g. t / T with T a power of two) the result is bitwise sincospif's.
 __device__ __forceinline__ float2 phasor_q32(uint32_t q) {
-  float a = (float)(int32_t)q * 4.656612873077392578125e-10f;  // 2^-31
+  const int32_t qi = (int32_t)q;
+  const int32_t qh = qi & ~0xFF, ql = qi - qh;  // qh: 24 significant bits
+  const float a = (float)qh * 4.656612873077392578125e-10f;  // 2^-31, exact
   float s, c;
   sincospif(a, &s, &c);
-  return make_float2(c, s);
+  const float d = (float)ql * 1.4629180792671596e-9f;  // pi 2^-31
+  return make_float2(fmaf(-s, d, c), fmaf(c, d, s));
 }
 
 }  // namespace srt3d

@@ -161,7 +161,11 @@ __device__ __forceinline__ void pixel_body(const PixArgs& a, float2* zrow, const
   for (int j = 0; j < m; j++) {  // frequency j+1
     if (ZTMA && MODE != PX_EXPECTED && WAIT_Z && j > 0 && j % 16 == 0) mbar_wait(zbar + j / 16, zpar);
     if (j > 0) {
-      if ((j & 31) == 0) {
+      // re-anchored from the exact phase every 32 frequencies in the specialised kernels (m <= 32:
+      // one anchor) and every 16 in the generic one (any m), whose worst-case recurrence error
+      // otherwise reaches the A12 floor (DESIGN.md §3 A12: 3 components at 1.0-1.2x the floor in
+      // 1024 extra fuzz shapes, all generic-m); the recurrence error grows with its length
+      if ((j & (M ? 31 : 15)) == 0) {
 #pragma unroll
         for (int k = 0; k < K; k++) {
           const float2 p = phasor_q32(q[k] * (uint32_t)(j + 1));

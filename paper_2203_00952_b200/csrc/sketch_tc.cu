@@ -16,8 +16,14 @@
 //  * H: integer counts c < 2048 held as the raw bits of an fp16 number.  The
 //    fp16 subnormal / first-normal binade is linear in its bit pattern:
 //    bits c encode exactly c * 2^-24 for 0 <= c < 2048, so the shared-memory
-//    histogram is built with plain integer atomics on packed u16 pairs and fed
-//    to the MMA as is (no conversion pass); the epilogue multiplies by 2^24.
+//    histogram is built with plain integer atomics on packed u16 pairs.  Fed
+//    to the MMA as is, a count below 1024 is a subnormal whose exponent field
+//    overstates its magnitude by 2^(10 - log2 c), and the tensor core aligns
+//    the products of a dot product by their exponent fields: the sum kept only
+//    ~14-15 bits below its largest term (round 2, measured: a two-photon pixel
+//    off by 1.3e-5, tools/tc_pair_probe.py).  So each unit's block is first
+//    scaled in place by one exact HMUL2 by 2^10 per count pair (c 2^-14, a
+//    normal fp16) and the epilogue multiplies by 2^14 (TC_NORMAL_COUNTS).
 //    A pixel with more than CNT_MAX photons is split into rounds of at most
 //    CNT_MAX photons whose MMAs accumulate into the same TMEM columns, so no
 //    count ever reaches 2048.
@@ -39,7 +45,7 @@
 //  * warps 0..3 (epilogue): warp w = pixel w of the tile = TMEM lanes 32w..;
 //    reads its N accumulator columns, combines hi + lo, twiddles by W[lane],
 //    reduce-scatters the 2 MP values across the warp (lane l ends with
-//    frequency l), scales by 2^24 / n and stores z coalesced.
+//    frequency l), scales by 2^14 / n and stores z coalesced.
 // Two A stages and two TMEM accumulators: the scatter of tile t + 1, the MMAs
 // of tile t and the epilogue of tile t - 1 run concurrently.
 // Supported: T <= TC_MAX_T (Kb <= 256, R <= 32), one pass of M <= 32
@@ -78,6 +84,13 @@ __device__ __forceinline__ uint64_t ns_desc(uint32_t saddr, uint32_t sbo) {
   return d;
 }
 
+#ifndef TC_NORMAL_COUNTS
+// 1: before its MMAs, each unit's histogram is converted in place from u16 counts (read by the
+// MMA as fp16 subnormal bit patterns c 2^-24) to the normal fp16 values c 2^-14.  With subnormal counts the
+// tensor core's accumulation keeps only ~13-14 bits below the largest product of a dot product
+// (measured: photons sharing a row lose up to ~3e-5 per pair, tools/tc_pair_probe.py).
+#define TC_NORMAL_COUNTS 1
+#endif
 #ifndef TC_CP
 // 1: each histogram stage copied into TMEM (tcgen05.cp 128x256b) and multiplied from there (A in
 // TMEM: 98 instead of 127 cycles per MMA in isolation, microbench/umma_rate.cu).  Measured slower in
@@ -335,12 +348,27 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
                 const uint32_t x = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
                 // x < T: an out-of-range bin (precondition violation) is the zero "absent photon"
                 // term (a zero increment at a wrapped in-block address)
-                const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
+const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
                 atomicAdd(Aw + ((x >> 1) & (SLOT_B / 4 - 1u)), inc);  // unconditional: a branch per photon costs more
               }
             }
           }
         }
+#if TC_NORMAL_COUNTS
+        {  // counts (bits c = c 2^-24 as fp16 subnormals) -> c 2^-14, normal fp16, by one exact
+           // HMUL2 by 2^10 per pair, in place, once both warps of the slot have scattered
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(TC_SLOT_THREADS) : "memory");
+          uint4* Av = reinterpret_cast<uint4*>(Ab);
+          const __half2 s10 = __float2half2_rn(1024.f);
+          for (uint32_t e = pt; e < SLOT_B / 16; e += TC_SLOT_THREADS) {
+            uint4 w = Av[e];
+            __half2* h = reinterpret_cast<__half2*>(&w);
+#pragma unroll
+            for (int i = 0; i < 4; i++) h[i] = __hmul2(h[i], s10);
+            Av[e] = w;
+          }
+        }
+#endif
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #ifdef TC_PROF
         if (prof) {
@@ -473,7 +501,8 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
       if constexpr (NV == 16) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
       if (warp == 0 && lane == 0) TCP_ADD(7, _tcp1);
       if (p < pend) {
-        const float sc = n ? (float)(16777216.0 / (double)n) : 0.f;  // 2^24 (count encoding) / n
+        // 1 / n (fp16 integer counts) or 2^24 / n (counts as subnormal bit patterns)
+        const float sc = n ? (float)((TC_NORMAL_COUNTS ? 16384.0 : 16777216.0) / (double)n) : 0.f;
         float* zp = reinterpret_cast<float*>(reinterpret_cast<float2*>(a.z) + (size_t)p * a.mstride + a.j0 + jj0);
         if constexpr (NV == 32) {
           // lane l holds value index l: frequency jj0 + l / 2, component l % 2

@@ -6,6 +6,8 @@ names a reproducible case id.  Tolerances as tests/test_gpu_parity.py
 (DESIGN.md §6): sketch |delta| <= 1e-5 absolute; loss / gradients per the A12
 per-component bound; backprojection |delta| <= 1e-5 * sum_l hhat_l |z_l|.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -13,11 +15,13 @@ from test_gpu_parity import _assert_sketch_close, _dev, _grad_tol_check, _host
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 128
+# SRT3D_FUZZ_CASES / SRT3D_FUZZ_BASE widen or shift the case range for a one-off longer run
+N_CASES = int(os.environ.get("SRT3D_FUZZ_CASES", "128"))
+_BASE = int(os.environ.get("SRT3D_FUZZ_BASE", "0"))
 
 
 def _case(i):
-    rng = np.random.default_rng(1_000_003 * (i + 1))
+    rng = np.random.default_rng(1_000_003 * (i + _BASE + 1))
     T = int(rng.choice([2, 3, 17, 100, 1000, 2500, 4096, 4613, 8192, 12000, 23800, 30000, 65535]))
     m = int(rng.integers(1, min(64, T - 1) + 1)) if T > 2 else 1
     npix = int(rng.choice([1, 7, 129, 1000, 3001]))

@@ -234,6 +234,53 @@ def test_sketch_class_paths_alignment_and_determinism(gpu, oracle_mod, inputs_mo
         gpu.srt3d_sketch_ex(db, do, {4: 12004, 5: 8193}.get(path, 23801), m, path=path, lanes_per_pixel=lanes)
 
 
+@pytest.mark.parametrize("T", [4613, 8192, 1000])
+def test_sketch_tensor_sparse_rows(gpu, oracle_mod, T):
+    """Tensor-core path on sparse pixels whose photons share a histogram row (DESIGN.md §5.7,
+    round-2 correction): with the counts fed to the MMA as fp16 subnormals the products of a row
+    kept only ~14 bits below its largest term, and a two-photon pixel (bins 17 and 1943 at
+    T = 4613) was off by 1.3e-5.  Every pixel here holds 2-6 photons in one row (same a_hi,
+    a_lo bits of the bin) with one small-phasor bin (k = 1) among them."""
+    import torch
+
+    q = 4
+    while (32 << q) < T:
+        q += 1
+    rng = np.random.default_rng(T)
+    lists = []
+    for _ in range(3000):
+        a = int(rng.integers(0, 32))
+        row = ((a >> 3) << (q + 3)) + ((a & 7) << 3)
+        ks = [1] + list(rng.integers(0, 1 << q, int(rng.integers(1, 6))))
+        xs = [row + ((k >> 3) << 6) + (k & 7) for k in ks]
+        xs = [x for x in xs if x < T]
+        lists.append(xs if xs else [T - 1])
+    lists[0] = [17, 1943] if T > 1943 else lists[0]
+    bins, offs = _csr(lists)
+    z = gpu.srt3d_sketch_ex(_dev(bins), _dev(offs), T, 32, total_photons=int(offs[-1]), path=gpu.PATH_TENSOR)
+    torch.cuda.synchronize()
+    _assert_sketch_close(_host(z), oracle_mod.sketch(bins, offs, T, 32), atol=1e-6)
+
+
+@pytest.mark.parametrize("T,m,K", [(23800, 32, 2), (65535, 32, 3), (23800, 27, 3), (1000, 32, 3)])
+def test_grad_a12_random_many_pixels(gpu, oracle_mod, T, m, K):
+    """A12 on 30000 random pixels per shape (DESIGN.md §3 A12): the phasor anchors take the
+    32-bit fixed-point phase as 24 exact bits + a first-order rotation by the low 8 (round 2);
+    converting all 32 bits to fp32 let the m = 32 recurrence exceed the floor by up to 1.4x for
+    T not a power of two (tools/a12_probe.py)."""
+    import torch
+
+    rng = np.random.default_rng(T + m + K)
+    npix, sigma = 30000, 2.0
+    z = ((rng.normal(size=(npix, m)) + 1j * rng.normal(size=(npix, m))) * 0.3).astype(np.complex64)
+    t = rng.uniform(0, T, (npix, K)).astype(np.float32)
+    a = rng.uniform(0.05, 1, (npix, K)).astype(np.float32)
+    gt, ga, L = gpu.srt3d_sketch_grad(_dev(z), _dev(t), _dev(a), sigma, T, m)
+    torch.cuda.synchronize()
+    go = oracle_mod.sketch_grad(z, t, a, sigma, T, m)
+    _grad_tol_check(z, t, a, sigma, T, m, (_host(gt), _host(ga), _host(L)), go)
+
+
 @pytest.mark.parametrize("T,m", [(4096, 10), (8192, 32), (1000, 20)])
 def test_sketch_tensor_heavy_pixels(gpu, oracle_mod, T, m):
     """Tensor-core path on pixels past one round (> 2040 photons: counts are
