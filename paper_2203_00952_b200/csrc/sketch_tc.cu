@@ -34,8 +34,8 @@
 //  * W[a][j] = e^{i w_j Kb a} from the exact phase index (j Kb a) mod T in
 //    fp64, rounded to fp32.
 //
-// Roles (one persistent CTA per SM, 13 warps):
-//  * warps 4..11 (builders): per unit (a tile of 4 pixels, or one round of a
+// Roles (one persistent CTA per SM, 8 + 4 TC_BLD_PER_SLOT + 1 warps):
+//  * warps 8.. (builders, TC_BLD_PER_SLOT per pixel slot): per unit (a tile of 4 pixels, or one round of a
 //    heavy tile) zero an A stage, scatter the photons into it with shared-
 //    memory atomics (16-byte vector loads of the tile's contiguous CSR range,
 //    issued one tile ahead), fence to the async proxy, arrive on full[s];
@@ -62,12 +62,16 @@ namespace srt3d {
 namespace {
 
 constexpr int TC_EPI_WARPS = 8;                 // two per pixel slot: warp w reads TMEM lanes 32 (w % 4), frequency half w / 4
-constexpr int TC_BLD_WARPS = 8;                 // two per pixel slot of a tile
-constexpr int TC_SLOT_THREADS = 64;
+#ifndef TC_BLD_PER_SLOT
+#define TC_BLD_PER_SLOT 4  // 4 builder warps per slot: C5 1.04 -> 0.94 ms (2: 96 regs; 4: 80; 5 spills, 1.26 ms)
+#endif
+constexpr int TC_BLD_WARPS = 4 * TC_BLD_PER_SLOT;  // builder warps per pixel slot of a tile
+constexpr int TC_SLOT_THREADS = 32 * TC_BLD_PER_SLOT;
 constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_BLD_WARPS;
 constexpr int TC_THREADS_ALL = (TC_MMA_WARP + 1) * 32;
 constexpr uint32_t CNT_MAX = 2040;      // photons of one pixel per round: every count < 2048, <= 256 groups
-constexpr int PF = 4;                   // 16-byte photon groups per builder thread (64 x 4 x 8 >= CNT_MAX + 7)
+// 16-byte photon groups per builder thread: a round's <= CNT_MAX photons span <= 256 groups
+constexpr int PF = (256 + TC_SLOT_THREADS - 1) / TC_SLOT_THREADS;
 // per-unit flags (builders -> MMA issuer, through shared memory under the full barrier)
 constexpr uint32_t TC_TPC_MAX = 768;  // tiles per CTA per launch (offsets staged in shared memory)
 constexpr uint32_t UF_FIRST = 1, UF_LAST = 2, UF_END = 4, UF_TB = 8;
@@ -271,9 +275,9 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
   const uint32_t tmem = tmem_slot;
 
   if (warp >= TC_EPI_WARPS && warp < TC_MMA_WARP) {
-    // ======================= builders: warps 8 + 2k, 9 + 2k own pixel slot k =======================
-    const uint32_t slot = (uint32_t)(warp - TC_EPI_WARPS) >> 1;
-    const uint32_t pt = (uint32_t)tid & 63u;
+    // ======================= builders: warps 8 + B k .. 8 + B k + B - 1 own pixel slot k (B = TC_BLD_PER_SLOT) ====
+    const uint32_t slot = (uint32_t)(warp - TC_EPI_WARPS) / TC_BLD_PER_SLOT;
+    const uint32_t pt = (uint32_t)(tid - TC_EPI_WARPS * 32) - slot * TC_SLOT_THREADS;
     const uint32_t esh = (uint32_t)(reinterpret_cast<uintptr_t>(a.bins) >> 1) & 7u;  // elements before 16 B alignment
     const uint4* gb = reinterpret_cast<const uint4*>(a.bins - esh);
     // the photon range [b0, b1) of this slot's pixel of local tile lt, round r
