@@ -344,22 +344,38 @@ __global__ void __launch_bounds__(512) coarse_count_kernel(const uint32_t* __res
   const unsigned long long c0 = (unsigned long long)blockIdx.x * BK_CHUNK;
   const unsigned long long c1 = min(nev, c0 + BK_CHUNK);
   uint32_t drop = 0;
-  for (unsigned long long e0 = c0 + threadIdx.x; e0 < c1; e0 += 8 * blockDim.x) {  // 8 loads in flight
-    uint32_t p[8];
+  auto count = [&](uint32_t p) {
+    if ((long long)p < npix)
+      atomicAdd(&h[p >> S], 1u);
+    else
+      drop++;
+  };
+  // 16-byte loads (four events each, four in flight per thread) over the chunk's aligned body
+  // (chunks start at multiples of 4 events: a 16-byte-aligned pix makes every chunk aligned);
+  // the scalar loop takes the chunk's last < 4 events, or everything if pix is misaligned
+  unsigned long long v1 = c0;
+  if ((reinterpret_cast<uintptr_t>(pix) & 15u) == 0) {
+    const uint4* pv = reinterpret_cast<const uint4*>(pix + c0);
+    const unsigned long long nv = (c1 - c0) >> 2;
+    for (unsigned long long i0 = threadIdx.x; i0 < nv; i0 += 4ull * blockDim.x) {
+      uint4 w[4];
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const unsigned long long e = e0 + q * blockDim.x;
-      p[q] = e < c1 ? __ldcs(pix + e) : 0xffffffffu;
-    }
+      for (int q = 0; q < 4; q++) {
+        const unsigned long long i = i0 + (unsigned long long)q * blockDim.x;
+        w[q] = i < nv ? __ldcs(pv + i) : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      }
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      if (e0 + q * blockDim.x >= c1) break;
-      if ((long long)p[q] < npix)
-        atomicAdd(&h[p[q] >> S], 1u);
-      else
-        drop++;
+      for (int q = 0; q < 4; q++) {
+        if (i0 + (unsigned long long)q * blockDim.x >= nv) break;
+        count(w[q].x);
+        count(w[q].y);
+        count(w[q].z);
+        count(w[q].w);
+      }
     }
+    v1 = c0 + 4 * nv;
   }
+  for (unsigned long long e = v1 + threadIdx.x; e < c1; e += blockDim.x) count(__ldcs(pix + e));
   __syncthreads();
   for (int b = threadIdx.x; b < NB; b += blockDim.x) table[(long long)b * nch + blockIdx.x] = h[b];
   if (drop) atomicAdd(dropped, drop);
