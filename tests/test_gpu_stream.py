@@ -60,6 +60,28 @@ def test_bucket_events_parity(gpu, oracle_mod, npix, T, n_ev, bad):
         assert np.array_equal(out[np.lexsort((out, seg))], ob[np.lexsort((ob, seg))])
 
 
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_bucket_events_alignment_and_tails(gpu, oracle_mod, offset):
+    """Pass A reads the pixel ids with 16-byte loads when the buffer is 16-byte aligned and
+    element by element otherwise: a pixel buffer starting 0-3 elements into an
+    allocation, an event count with a ragged last chunk (n mod 4 != 0), dropped events."""
+    import torch
+
+    npix, T, n_ev = 70001, 2048, 3 * 32768 + 4097
+    p, b = _events(npix, T, n_ev, seed=offset + 11, extra_bad=3)
+    dp = torch.zeros(p.size + 4, dtype=torch.int32, device="cuda")
+    db = torch.zeros(b.size + 4, dtype=torch.int16, device="cuda")
+    dp[offset: offset + p.size] = _dev(p.view(np.int32))
+    db[offset: offset + b.size] = _dev(b.view(np.int16))
+    pv = dp[offset: offset + p.size].view(torch.uint32)
+    bv = db[offset: offset + b.size].view(torch.uint16)
+    offs, out, dropped = gpu.srt3d_bucket_events(pv, bv, npix)
+    torch.cuda.synchronize()
+    oo, ob, od = oracle_mod.bucket_events(p, b, npix)
+    assert np.array_equal(offs.cpu().numpy(), oo) and int(dropped.item()) == od == 3
+    assert np.array_equal(out.cpu().numpy()[: int(oo[-1])], ob)
+
+
 @pytest.mark.parametrize("T,m", [(8192, 32), (4613, 10), (1024, 4)])
 def test_events_to_sketch(gpu, oracle_mod, T, m):
     import torch
