@@ -95,6 +95,12 @@ __device__ __forceinline__ uint64_t ns_desc(uint32_t saddr, uint32_t sbo) {
 // (measured: photons sharing a row lose up to ~3e-5 per pair, tools/tc_pair_probe.py).
 #define TC_NORMAL_COUNTS 1
 #endif
+#ifndef TC_TMEM_A
+// 1: the builders convert each unit's counts straight into a TMEM A stage (tcgen05.st) and zero the
+// shared-memory histogram in the same pass; the MMAs read A from TMEM (the histogram is never an
+// MMA operand, so one shared-memory stage suffices and the separate zeroing pass disappears)
+#define TC_TMEM_A 1  // C5 0.936 -> 0.929 ms, C2 0.077 -> 0.066 ms (measured round 2)
+#endif
 #ifndef TC_CP
 // 1: each histogram stage copied into TMEM (tcgen05.cp 128x256b) and multiplied from there (A in
 // TMEM: 98 instead of 127 cycles per MMA in isolation, microbench/umma_rate.cu).  Measured slower in
@@ -138,6 +144,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -265,7 +276,7 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
-                 "r"(TC_CP ? 512u : 2u * N));
+                 "r"((TC_CP || TC_TMEM_A) ? 512u : 2u * N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -276,8 +287,15 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
 
   if (warp >= TC_EPI_WARPS && warp < TC_MMA_WARP) {
     // ======================= builders: warps 8 + B k .. 8 + B k + B - 1 own pixel slot k (B = TC_BLD_PER_SLOT) ====
+#if TC_TMEM_A
+    // slot k = builder warps 8 + k, 12 + k, ...: warp % 4 == k, the TMEM lane quarter of the slot's rows
+    const uint32_t slot = (uint32_t)(warp - TC_EPI_WARPS) & 3u;
+    const uint32_t wi = (uint32_t)(warp - TC_EPI_WARPS) >> 2;  // warp within the slot
+    const uint32_t pt = wi * 32u + (uint32_t)lane;
+#else
     const uint32_t slot = (uint32_t)(warp - TC_EPI_WARPS) / TC_BLD_PER_SLOT;
     const uint32_t pt = (uint32_t)(tid - TC_EPI_WARPS * 32) - slot * TC_SLOT_THREADS;
+#endif
     const uint32_t esh = (uint32_t)(reinterpret_cast<uintptr_t>(a.bins) >> 1) & 7u;  // elements before 16 B alignment
     const uint4* gb = reinterpret_cast<const uint4*>(a.bins - esh);
     // the photon range [b0, b1) of this slot's pixel of local tile lt, round r
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
       const uint32_t rounds = rounds_s[lt];
       for (uint32_t r = 0; r < rounds; r++, unit++) {
         const uint32_t s = unit & 1u;
-        unsigned char* Ab = A0 + s * ASZ + slot * SLOT_B;
+        unsigned char* Ab = A0 + (TC_TMEM_A ? 0u : s * ASZ) + slot * SLOT_B;  // TMEM A: one histogram stage
         if (r > 0) load_groups(lt, r, cur);  // heavy pixel rounds: this round's groups now
         if (r == 0 && lt + 2 < ntl) load_groups(lt + 2, 0, dst);
         uint32_t b0, b1;
@@ -323,7 +341,7 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
         const bool prof = tid == TC_EPI_WARPS * 32;
         long long c0 = clock64(), c1 = c0, c2 = c0;
 #endif
-        if (unit >= 2) {
+        if (!TC_TMEM_A && unit >= 2) {
           mbar_wait(&empty_bar[s], ((unit >> 1) - 1u) & 1u);  // MMAs of unit - 2 done with this stage
 #ifdef TC_PROF
           c1 = clock64();
@@ -358,7 +376,39 @@ const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
             }
           }
         }
-#if TC_NORMAL_COUNTS
+#if TC_TMEM_A
+        {  // counts -> normal fp16 (c 2^-14, HMUL2 by 2^10) straight into TMEM A stage s: lane = row
+           // a of this slot's pixel, warp wi takes 16-element K groups wi, wi + 4, ...; each 16-byte
+           // chunk is zeroed as it is read (the next unit scatters into the same histogram)
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(TC_SLOT_THREADS) : "memory");
+          if (unit >= 2) mbar_wait(&empty_bar[s], ((unit >> 1) - 1u) & 1u);  // MMAs of unit - 2 read stage s
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const __half2 s10 = __float2half2_rn(1024.f);
+          const uint32_t rowb = (uint32_t)(lane >> 3) * 16u * Kb + (uint32_t)(lane & 7) * 16u;
+          const uint32_t ta = tmem + ((slot * 32u) << 16) + 2u * (uint32_t)N + s * (Kb >> 1);
+          for (uint32_t g = wi; g < Kb / 16u; g += TC_BLD_PER_SLOT) {
+            uint32_t rr[8];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {  // k_hi = 2 g + h
+              uint4* cp = reinterpret_cast<uint4*>(Ab + rowb + (2u * g + (uint32_t)h) * 128u);
+              uint4 w = *cp;
+              *cp = make_uint4(0u, 0u, 0u, 0u);
+              __half2* hh = reinterpret_cast<__half2*>(&w);
+#pragma unroll
+              for (int i = 0; i < 4; i++) hh[i] = __hmul2(hh[i], s10);
+              rr[4 * h + 0] = w.x;
+              rr[4 * h + 1] = w.y;
+              rr[4 * h + 2] = w.z;
+              rr[4 * h + 3] = w.w;
+            }
+            tmem_st8(ta + 8u * g, rr);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          // every chunk read and zeroed before any warp of the slot scatters the next unit
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(TC_SLOT_THREADS) : "memory");
+        }
+#elif TC_NORMAL_COUNTS
         {  // counts (bits c = c 2^-24 as fp16 subnormals) -> c 2^-14, normal fp16, by one exact
            // HMUL2 by 2^10 per pair, in place, once both warps of the slot have scattered
           asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(TC_SLOT_THREADS) : "memory");
@@ -435,6 +485,11 @@ const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
           mma_f16_ts(tmem + tb * (uint32_t)N, ta + kk * 8u, ns_desc(sb + kk * 256u, SBO), idesc,
                      (!(f & UF_FIRST) || kk > 0) ? 1u : 0u);
         commit(&afree_bar[s]);
+#elif TC_TMEM_A
+        for (uint32_t kk = 0; kk < Kb / 16; kk++)  // A: TMEM stage s, 8 columns (16 fp16) per K step
+          mma_f16_ts(tmem + tb * (uint32_t)N, tmem + 2u * (uint32_t)N + s * (Kb >> 1) + kk * 8u,
+                     ns_desc(sb + kk * 256u, SBO), idesc, (!(f & UF_FIRST) || kk > 0) ? 1u : 0u);
+        commit(&empty_bar[s]);
 #else
         for (uint32_t kk = 0; kk < Kb / 16; kk++)  // K step of 16 = two core matrices along K
           mma_f16(tmem + tb * (uint32_t)N, ns_desc(sa + kk * 256u, SBO), ns_desc(sb + kk * 256u, SBO), idesc,
@@ -522,7 +577,7 @@ const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_CP ? 512u : 2u * N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((TC_CP || TC_TMEM_A) ? 512u : 2u * N));
 }
 
 template <int MP>
