@@ -95,6 +95,9 @@ __device__ __forceinline__ uint64_t ns_desc(uint32_t saddr, uint32_t sbo) {
 // (measured: photons sharing a row lose up to ~3e-5 per pair, tools/tc_pair_probe.py).
 #define TC_NORMAL_COUNTS 1
 #endif
+#ifndef TC_LATE_PREFETCH
+#define TC_LATE_PREFETCH 1
+#endif
 #ifndef TC_TMEM_A
 // 1: the builders convert each unit's counts straight into a TMEM A stage (tcgen05.st) and zero the
 // shared-memory histogram in the same pass; the MMAs read A from TMEM (the histogram is never an
@@ -334,7 +337,9 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
         const uint32_t s = unit & 1u;
         unsigned char* Ab = A0 + (TC_TMEM_A ? 0u : s * ASZ) + slot * SLOT_B;  // TMEM A: one histogram stage
         if (r > 0) load_groups(lt, r, cur);  // heavy pixel rounds: this round's groups now
+#if !TC_LATE_PREFETCH
         if (r == 0 && lt + 2 < ntl) load_groups(lt + 2, 0, dst);
+#endif
         uint32_t b0, b1;
         range(lt, r, b0, b1);
 #ifdef TC_PROF
@@ -376,6 +381,11 @@ const uint32_t inc = (((msk >> e) & 1u) & (uint32_t)(x < T)) << ((x & 1u) << 4);
             }
           }
         }
+#if TC_LATE_PREFETCH
+        // tile lt + 2's groups issued only after this tile's registers were consumed: issued at the top
+        // of the body they shared scoreboards with them, and the scatter waited for the new loads too
+        if (r == 0 && lt + 2 < ntl) load_groups(lt + 2, 0, dst);
+#endif
 #if TC_TMEM_A
         {  // counts -> normal fp16 (c 2^-14, HMUL2 by 2^10) straight into TMEM A stage s: lane = row
            // a of this slot's pixel, warp wi takes 16-element K groups wi, wi + 4, ...; each 16-byte
