@@ -34,20 +34,24 @@
 //  * W[a][j] = e^{i w_j Kb a} from the exact phase index (j Kb a) mod T in
 //    fp64, rounded to fp32.
 //
-// Roles (one persistent CTA per SM, 8 + 4 TC_BLD_PER_SLOT + 1 warps):
-//  * warps 8.. (builders, TC_BLD_PER_SLOT per pixel slot): per unit (a tile of 4 pixels, or one round of a
-//    heavy tile) zero an A stage, scatter the photons into it with shared-
-//    memory atomics (16-byte vector loads of the tile's contiguous CSR range,
-//    issued one tile ahead), fence to the async proxy, arrive on full[s];
-//  * warp 12, one thread (MMA issuer): waits full[s] (and the TMEM buffer's
-//    accempty), issues 4 KA tcgen05.mma, commits to empty[s] (A stage free)
-//    and, after a tile's last round, to accfull[tb];
-//  * warps 0..3 (epilogue): warp w = pixel w of the tile = TMEM lanes 32w..;
-//    reads its N accumulator columns, combines hi + lo, twiddles by W[lane],
-//    reduce-scatters the 2 MP values across the warp (lane l ends with
-//    frequency l), scales by 2^14 / n and stores z coalesced.
-// Two A stages and two TMEM accumulators: the scatter of tile t + 1, the MMAs
-// of tile t and the epilogue of tile t - 1 run concurrently.
+// Roles (one persistent CTA per SM, 8 epilogue + 4 TC_BLD_PER_SLOT builder + 1 MMA warps):
+//  * builders (warps 8.., TC_BLD_PER_SLOT per pixel slot; with TC_TMEM_A slot k is
+//    warps 8 + k, 12 + k, ... so that warp % 4 is the slot's TMEM lane quarter):
+//    per unit (a tile of 4 pixels, or one round of a heavy tile) scatter the
+//    photons into the slot's shared-memory histogram with integer atomics
+//    (16-byte vector loads of the tile's contiguous CSR range, issued after the
+//    previous tile's scatter, two tiles ahead), then convert the counts to
+//    normal fp16 (HMUL2 by 2^10) straight into TMEM A stage s with tcgen05.st,
+//    zeroing the histogram as it is read, and arrive on full[s];
+//  * the MMA warp, one thread: waits full[s] (and the TMEM accumulator's
+//    accempty), issues Kb/16 tcgen05.mma with A from TMEM, commits to empty[s]
+//    (A stage free) and, after a tile's last round, to accfull[tb];
+//  * epilogue (warps 0..7: pixel slot w % 4, frequency half w / 4): reads its
+//    accumulator columns, combines hi + lo, twiddles by W[lane],
+//    reduce-scatters across the warp (lane l ends with frequency l), scales by
+//    2^14 / n and stores z coalesced.
+// Two TMEM A stages and two TMEM accumulators: the scatter of tile t + 1, the
+// MMAs of tile t and the epilogue of tile t - 1 run concurrently.
 // Supported: T <= TC_MAX_T (Kb <= 256, R <= 32), one pass of M <= 32
 // frequencies (MP = 16 for M <= 16, else 32).
 #include <cuda_fp16.h>
@@ -103,6 +107,9 @@ __device__ __forceinline__ uint64_t ns_desc(uint32_t saddr, uint32_t sbo) {
 // shared-memory histogram in the same pass; the MMAs read A from TMEM (the histogram is never an
 // MMA operand, so one shared-memory stage suffices and the separate zeroing pass disappears)
 #define TC_TMEM_A 1  // C5 0.936 -> 0.929 ms, C2 0.077 -> 0.066 ms (measured round 2)
+#endif
+#if defined(TC_CP) && TC_CP && TC_TMEM_A
+#error "TC_CP (tcgen05.cp of shared-memory stages) and TC_TMEM_A (tcgen05.st of converted counts) exclude each other"
 #endif
 #ifndef TC_CP
 // 1: each histogram stage copied into TMEM (tcgen05.cp 128x256b) and multiplied from there (A in
