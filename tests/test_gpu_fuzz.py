@@ -132,9 +132,11 @@ def test_fuzz_init_depths(gpu, oracle_mod, inputs_mod, i):
     # every pixel where the picks differ is checked to be a valid greedy choice within tolerance
     # (_check_picks raises otherwise); their number is bounded except on shapes where ties are
     # structural: T < 8 (T = 2, N = 3: g_1 = g_2 exactly, the fp64 oracle breaks the tie by
-    # rounding) or N <= 2m (a grid no finer than the sketch's band: neighbouring grid values of
-    # g coincide to rounding)
+    # rounding), N <= 2m (a grid no finer than the sketch's band: neighbouring grid values of
+    # g coincide to rounding) or 2m > T (frequencies past T/2 alias, z_{T-j} = conj(z_j) exactly
+    # for integer bins, so g carries near-symmetric pairs of maxima: an extended fuzz run found
+    # 60 of 1000 valid-but-different picks at T = 100, m = 56)
     bad = _check_picks(tg, cg, 2e-5 * S, to.astype(np.float32), co, lambda r: gfull[r], T, N, min_sep)
-    if T >= 8 and N > 2 * m:
+    if T >= 8 and N > 2 * m and 2 * m <= T:
         assert bad <= max(2, npix // 20), (c, N, min_sep, bad)
     assert np.all((_host(ag) >= 0) & (_host(ag) <= 1)) and np.all(cg <= K)
