@@ -227,14 +227,38 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- one-time setup: B (hi | lo split), W, zeroed A stages, barriers, TMEM ----
+  // V[k][j] = e^{i w_j X_col(k)}, X_col(k) = 64 k_hi + k_lo, as the fp64 product of
+  // e^{i w_j 64 k_hi} and e^{i w_j k_lo} (40 sincospi per frequency instead of Kb; the
+  // product's rounding, ~1e-16, is far below the fp16 hi/lo split's 2^-24), the factors staged
+  // in the (not yet used) histogram region
+  // (Kb >= 64: the region holds the 40 MP factors; smaller blocks take sincospi per entry)
+  double2* vf = reinterpret_cast<double2*>(A0);  // [MP][40]: k_hi = 0..31, then k_lo = 0..7
+  const bool vfact = 2u * ASZ >= (uint32_t)MP * 40u * (uint32_t)sizeof(double2);
+  for (uint32_t e = tid; vfact && e < (uint32_t)MP * 40u; e += TC_THREADS_ALL) {
+    const uint32_t jj = e / 40u, i = e % 40u;
+    double2 v = make_double2(0.0, 0.0);
+    if (jj < M && (i >= 32u || i < (Kb >> 3))) {
+      const uint32_t j = a.j0 + 1u + jj;
+      const uint32_t xc = i < 32u ? 64u * i : i - 32u;
+      const uint32_t r = (uint32_t)(((unsigned long long)j * xc) % T);
+      sincospi(2.0 * (double)r / (double)T, &v.y, &v.x);
+    }
+    vf[e] = v;
+  }
+  __syncthreads();
   for (uint32_t e = tid; e < (uint32_t)MP * Kb; e += TC_THREADS_ALL) {
     const uint32_t jj = e >> q, k = e & (Kb - 1u);
     __half h[4] = {__float2half(0.f), __float2half(0.f), __float2half(0.f), __float2half(0.f)};
     if (jj < M) {
-      const uint32_t j = a.j0 + 1u + jj;
-      const uint32_t r = (uint32_t)(((unsigned long long)j * tc_xcol(k)) % T);
-      double sn, c;
-      sincospi(2.0 * (double)r / (double)T, &sn, &c);
+      double c, sn;
+      if (vfact) {
+        const double2 ph = vf[jj * 40u + (k >> 3)], pl = vf[jj * 40u + 32u + (k & 7u)];
+        c = ph.x * pl.x - ph.y * pl.y;
+        sn = ph.x * pl.y + ph.y * pl.x;
+      } else {
+        const uint32_t r = (uint32_t)(((unsigned long long)(a.j0 + 1u + jj) * tc_xcol(k)) % T);
+        sincospi(2.0 * (double)r / (double)T, &sn, &c);
+      }
       const __half ch = __double2half(c), sh = __double2half(sn);
       h[0] = ch;
       h[1] = sh;
@@ -259,6 +283,7 @@ __global__ void __launch_bounds__(TC_THREADS_ALL, 1)
     }
     Ws[e] = w;
   }
+  __syncthreads();  // every V product read its factors before the histogram region is zeroed
   for (uint32_t e = tid; e < 2 * ASZ / 16; e += TC_THREADS_ALL)
     reinterpret_cast<uint4*>(A0)[e] = make_uint4(0u, 0u, 0u, 0u);
   // this CTA's tiles: [t0, t0 + ntl) of the launch's ceil(pcount / 4); its pixels' offsets staged
