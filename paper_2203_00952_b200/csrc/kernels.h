@@ -24,6 +24,10 @@ constexpr int PX_THREADS = 128;                 // pixel-kernel CTA size
 #define GRAD_PERSIST 0  // 1: one wave of TMA-gradient CTAs, each warp looping over tiles (measured slower:
                         // C5 22.4 us cold, 16.4 in loop vs 18.0 / 13.55 — per-warp tiles in sequence expose the loads)
 #endif
+#ifndef GRAD_PDL_TRIGGER
+#define GRAD_PDL_TRIGGER 0  // 1: each TMA-gradient CTA fires griddepcontrol.launch_dependents once its tile
+                            // loads are issued, so the next step's CTAs are scheduled during this one's tail
+#endif
 #ifndef GRAD_MIN_BLOCKS
 #define GRAD_MIN_BLOCKS 12                       // smem caps residency at 12 CTAs/SM: let ptxas use up to 80 regs
 #endif

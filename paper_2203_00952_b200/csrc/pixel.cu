@@ -348,6 +348,9 @@ __global__ void __launch_bounds__(GRAD_THREADS, GRAD_TMA_MIN_BLOCKS) grad_kernel
       }
     }
     __syncwarp();
+    // scheduling only: the dependent step still waits (griddepcontrol.wait) for this grid to
+    // complete before it reads anything
+    if (GRAD_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     float gt[K], ga[K], L;
     pixel_body<K, M, MODE, true, true>(a, reinterpret_cast<float2*>(tile + lane * 128), nullptr, nullptr, tk, ak, gt,
                                        ga, L, bar, par);
