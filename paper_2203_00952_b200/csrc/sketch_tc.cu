@@ -67,7 +67,8 @@ namespace {
 
 constexpr int TC_EPI_WARPS = 8;                 // two per pixel slot: warp w reads TMEM lanes 32 (w % 4), frequency half w / 4
 #ifndef TC_BLD_PER_SLOT
-#define TC_BLD_PER_SLOT 4  // 4 builder warps per slot: C5 1.04 -> 0.94 ms (2: 96 regs; 4: 80; 5 spills, 1.26 ms)
+#define TC_BLD_PER_SLOT 3  // builder warps per slot: 2 -> 4: C5 1.04 -> 0.94 ms (2: 96 regs; 5 spills, 1.26 ms);
+                           // 4 -> 3 (80 regs, 672 threads): C5 0.883 -> 0.835-0.840 ms, C2 0.077 -> 0.078 ms
 #endif
 constexpr int TC_BLD_WARPS = 4 * TC_BLD_PER_SLOT;  // builder warps per pixel slot of a tile
 constexpr int TC_SLOT_THREADS = 32 * TC_BLD_PER_SLOT;
